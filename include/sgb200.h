@@ -1,0 +1,151 @@
+/* sgb200.h — C ABI of the B200-native estimation-based SpGEMM (libsgb200.so).
+ *
+ * Drop-in boundary for the reference's `sketchgemm.spgemm` pipeline
+ * (/root/reference/pkg/src/sketchgemm/engine.py:136-249).  The reference is a
+ * pure-Python package with no FFI; these entry points are the stage operators
+ * its engine calls, re-expressed as plain C over DEVICE pointers so that the
+ * Python host (paper_2604_19004_b200/engine.py) binds them with ctypes exactly
+ * as a maintainer would from sketchgemm.
+ *
+ * Conventions
+ *  - every pointer is a device pointer unless named *_host;
+ *  - CSR: row_ptr int64[n+1], col_idx int32[nnz], values f64 (dtype 0) or
+ *    f32 (dtype 1); per-row arrays are int64 unless stated;
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream);
+ *  - return 0 on success, else an SG_ERR_* code; sg_last_error() gives the
+ *    message of the last failure on the calling thread;
+ *  - no global mutable state besides the per-thread error string: scratch is
+ *    passed in (`ws`, sized by sg_workspace_bytes), so calls are reentrant.
+ */
+#ifndef SGB200_H
+#define SGB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_OK 0
+#define SG_ERR_ARG 1
+#define SG_ERR_CUDA 2
+#define SG_ERR_WORKSPACE 3
+
+#define SG_F64 0
+#define SG_F32 1
+
+/* prediction kinds (predict.py:27-30) */
+#define SG_PRED_EXACT 0
+#define SG_PRED_ESTIMATED 1
+#define SG_PRED_UPPER 2
+
+/* plan kinds (accumulate.py:39-44) */
+#define SG_KIND_HASH 0
+#define SG_KIND_ENHANCED_HASH 1
+#define SG_KIND_DENSE 2
+#define SG_KIND_ESC 3
+#define SG_KIND_FALLBACK 4
+
+/* Tier ladder (accumulate.py:47-61). */
+typedef struct sg_tiers {
+  int32_t n_hash;
+  int32_t n_dense;
+  int64_t hash_caps[8];
+  int64_t dense_spans[8];
+  int64_t enh_cap;
+  int64_t esc_max;
+  double coef;
+} sg_tiers_t;
+
+int sg_abi_version(void);
+const char* sg_last_error(void);
+
+/* Number of kernels this library has enqueued since load (diagnostic;
+ * bench.py reports the count inside its timed region). */
+unsigned long long sg_launch_count(void);
+
+/* Scratch bytes needed by sg_symbolic / sg_numeric / sg_fallback / sg_scan
+ * for a problem with `m` rows of A. */
+size_t sg_workspace_bytes(int64_t m);
+
+/* Replaces analysis.compute_row_stats (analysis.py:96-128): products per row,
+ * output span [span_lo, span_hi] (sentinels b_ncols / -1 when a row has no
+ * products); totals2[0] = total products, totals2[1] = max row products. */
+int sg_row_stats(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col,
+                 const int64_t* b_ptr, const int32_t* b_col, int64_t* products,
+                 int64_t* span_lo, int64_t* span_hi, int64_t* totals2, void* stream);
+
+/* Replaces analysis.build_b_sketches (analysis.py:131-146) + hll.hash_ranks
+ * (hll.py:64-76): regs is uint8[k * 2^p], one HLL sketch per row of B. */
+int sg_hll_build(int64_t k, const int64_t* b_ptr, const int32_t* b_col, int p, uint8_t* regs,
+                 void* stream);
+
+/* Replaces analysis.merged_row_estimates (analysis.py:149-169) and
+ * predict.estimate_pass (predict.py:87-103): per selected row of A (rows ==
+ * NULL selects all nsel = m rows), max-merge the sketches of the B rows it
+ * selects and estimate (hll.py:79-86).  lin_table[z] = m*ln(m/z) for z in
+ * 1..m-1 (precomputed by the host with the reference's own log so the
+ * linear-counting branch is bit-identical); alpha_mm = (alpha_m*m)*m. */
+int sg_hll_estimate(int64_t nsel, const int64_t* rows, const int64_t* a_ptr,
+                    const int32_t* a_col, const uint8_t* regs, int p, const double* lin_table,
+                    double alpha_mm, double* est, void* stream);
+
+/* Replaces predict.symbolic_pass (predict.py:39-84): exact distinct output
+ * columns per row of C (counts int64[m]). */
+int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col,
+                const int64_t* b_ptr, const int32_t* b_col, const int64_t* products,
+                const int64_t* span_lo, const int64_t* span_hi, int64_t* counts, void* ws,
+                size_t ws_bytes, void* stream);
+
+/* Replaces accumulate.plan_rows (accumulate.py:104-181) with the identical
+ * integer rules.  pred is int64 (EXACT / UPPER) or f64 (ESTIMATED). */
+int sg_plan(int64_t m, int pred_kind, const void* pred, const int64_t* products,
+            const int64_t* span_lo, const int64_t* span_hi, const sg_tiers_t* tiers,
+            int8_t* kind, int64_t* cap, int64_t* alloc, void* stream);
+
+/* Exclusive prefix sum of int64 in[n] into out[n+1] (engine.py:256-258,349-350). */
+int sg_scan(int64_t n, const int64_t* in, int64_t* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Replaces engine._numeric_phase (engine.py:252-309) with the batch kernels
+ * accumulate_hash_like / accumulate_esc / accumulate_dense
+ * (accumulate.py:335-430): every row whose plan kind is not FALLBACK and that
+ * has products is accumulated and written SORTED at out_off[row] (hash rows
+ * are sorted in-kernel: engine._sort_hash_rows, engine.py:331-343).
+ * counts[row] = distinct count (0 if overflowed); overflow[row] = 1 when the
+ * reference's tier limit is exceeded (hash: count > floor(0.8*cap); dense:
+ * count > alloc). */
+int sg_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, const int32_t* a_col,
+               const void* a_val, const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
+               const int8_t* kind, const int64_t* cap, const int64_t* alloc,
+               const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
+               const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts,
+               uint8_t* overflow, void* ws, size_t ws_bytes, void* stream);
+
+/* Rows for the fallback pass (engine.py:202-203): overflow | (kind ==
+ * FALLBACK & products > 0), ascending; *n_out_host receives the count. */
+int sg_select_fallback(int64_t m, const int8_t* kind, const int64_t* products,
+                       const uint8_t* overflow, int64_t* rows_out, int64_t* n_out_host, void* ws,
+                       size_t ws_bytes, void* stream);
+
+/* Replaces engine._fallback_phase (engine.py:312-328) /
+ * accumulate.fallback_accumulate (accumulate.py:274-279): exact accumulation
+ * of the given rows, which can never overflow.  mode 0 = count only
+ * (counts[row] written), mode 1 = numeric, written sorted at out_off[row]. */
+int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, int dtype,
+                const int64_t* a_ptr, const int32_t* a_col, const void* a_val,
+                const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
+                const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
+                const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts,
+                void* ws, size_t ws_bytes, void* stream);
+
+/* Replaces engine.compact (engine.py:346-368): copy counts[row] entries of
+ * every row with skip[row] == 0 from src_off[row] to dst_off[row]. */
+int sg_compact(int64_t m, int dtype, const int64_t* counts, const uint8_t* skip,
+               const int64_t* src_off, const int64_t* dst_off, const int32_t* src_col,
+               const void* src_val, int32_t* dst_col, void* dst_val, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGB200_H */

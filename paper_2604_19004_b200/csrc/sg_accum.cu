@@ -1,0 +1,973 @@
+// sg_accum.cu — the accumulators: symbolic counting, numeric Gustavson pass,
+// fallback re-execution.  Hot path of the estimation-based SpGEMM.
+//
+// Reference semantics (all exact; only the summation order of values may
+// differ, as it already does between the reference's own bins):
+//   symbolic_pass            predict.py:39-84         -> count mode
+//   accumulate_hash_like     accumulate.py:335-365    -> hash families, limit floor(0.8 cap)
+//   accumulate_esc           accumulate.py:368-378    -> ESC family
+//   accumulate_dense         accumulate.py:381-430    -> bitmap family, limit alloc
+//   _fallback_phase          engine.py:312-328        -> bitmap family, no limit
+//   _sort_hash_rows          engine.py:331-343        -> fused: rows leave sorted
+//
+// GPU accumulator families (chosen per row by a classify kernel, rows grouped
+// into bins by a partition pass, one launch per non-empty bin):
+//   ESC  warp per row, <= 64 products in shared memory, bitonic sort + segment sum
+//   HW   warp per row, shared-memory open-addressing hash, T in [32, 2048]
+//   HB   block per row, shared-memory hash, T in [2048, 32768]
+//   BM   block per row, shared-memory bitmap over the row's column span (up to
+//        2^20 columns per window; wider spans loop over windows); count =
+//        popcount, output columns come out of the bitmap already sorted, values
+//        are accumulated with fire-and-forget fp64 REDs into the row's output
+//        slots at rank(col) — the paper's shared+global spill accumulator,
+//        with the key side held as a bitmap.
+// Product iteration is load balanced inside each row: A-row chunks are
+// prefix-summed over their B-row lengths and every warp walks a contiguous
+// range of products (CREDUX.OR finds segment owners), so a row with one hub
+// B row keeps all warps busy.
+#include <algorithm>
+#include <climits>
+#include <string>
+
+#include "sg_internal.cuh"
+
+namespace sg {
+
+constexpr int64_t NOLIMIT = 0x7fffffffffffffffll;
+
+struct Csr {
+  const int64_t* ptr;
+  const int32_t* col;
+  const void* val;
+};
+
+// -------------------------------------------------------------------------
+// product iteration
+
+// compacted non-empty A entries of one chunk (shared memory)
+struct Entries {
+  int64_t* S;   // first product index of the entry within the chunk (excl scan)
+  int64_t* bs;  // start of the B row
+  double* av;   // A value
+};
+
+__device__ __forceinline__ unsigned lanemask_le() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// The calling warp processes products [pbeg, pend) of a chunk; op(col, val).
+template <bool VALUES, typename V, class Op>
+__device__ __forceinline__ void warp_products(const Entries& E, int nent, int64_t pbeg, int64_t pend,
+                                              const int32_t* __restrict__ b_col,
+                                              const V* __restrict__ b_val, Op& op) {
+  if (pbeg >= pend) return;
+  const int lane = lane_id();
+  int lo = 0, hi = nent - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (E.S[mid] <= pbeg) lo = mid; else hi = mid - 1;
+  }
+  int c0 = lo;
+  const unsigned le = lanemask_le();
+  for (int64_t p0 = pbeg; p0 < pend; p0 += 32) {
+    const int ci = c0 + 1 + lane;
+    const int64_t nxt = ci < nent ? E.S[ci] : (int64_t)NOLIMIT;
+    const int64_t d = nxt - p0;
+    const unsigned bit = d < 32 ? (1u << (unsigned)d) : 0u;
+    const unsigned mask = __reduce_or_sync(SG_FULL, bit);
+    const int c = c0 + __popc(mask & le);
+    const int64_t p = p0 + lane;
+    if (p < pend) {
+      const int64_t j = E.bs[c] + (p - E.S[c]);
+      const int32_t col = __ldg(b_col + j);
+      double v = 0.0;
+      if (VALUES) v = E.av[c] * (double)__ldg(b_val + j);
+      op(col, v);
+    }
+    const int k = __popc(mask);
+    const int64_t nk = __shfl_sync(SG_FULL, nxt, k);
+    c0 = c0 + k + (nk == p0 + 32 ? 1 : 0);
+  }
+}
+
+// Load one chunk of A entries for a warp (CH = 32), compacting empties.
+// Returns the chunk's product total; nent receives the entry count.
+template <bool VALUES, typename V>
+__device__ __forceinline__ int64_t warp_load_chunk(int64_t t, int64_t t1, const int32_t* __restrict__ a_col,
+                                                   const V* __restrict__ a_val,
+                                                   const int64_t* __restrict__ b_ptr, Entries E, int& nent) {
+  const int lane = lane_id();
+  int64_t bs = 0, len = 0;
+  double av = 0.0;
+  if (t + lane < t1) {
+    const int32_t k = a_col[t + lane];
+    bs = b_ptr[k];
+    len = b_ptr[k + 1] - bs;
+    if (VALUES) av = (double)a_val[t + lane];
+  }
+  const int64_t incl = warp_incl_scan(len);
+  const unsigned nz = __ballot_sync(SG_FULL, len > 0);
+  const int pos = __popc(nz & lanemask_lt());
+  __syncwarp();
+  if (len > 0) {
+    E.S[pos] = incl - len;
+    E.bs[pos] = bs;
+    if (VALUES) E.av[pos] = av;
+  }
+  __syncwarp();
+  nent = __popc(nz);
+  return __shfl_sync(SG_FULL, incl, 31);
+}
+
+// Whole row with one warp.
+template <bool VALUES, typename V, class Op>
+__device__ __forceinline__ void warp_row(int64_t row, const int64_t* __restrict__ a_ptr,
+                                         const int32_t* __restrict__ a_col, const V* __restrict__ a_val,
+                                         const int64_t* __restrict__ b_ptr, const int32_t* __restrict__ b_col,
+                                         const V* __restrict__ b_val, Entries E, Op& op,
+                                         volatile int* stop) {
+  const int64_t t1 = a_ptr[row + 1];
+  for (int64_t t = a_ptr[row]; t < t1; t += 32) {
+    int nent;
+    const int64_t P = warp_load_chunk<VALUES, V>(t, t1, a_col, a_val, b_ptr, E, nent);
+    if (P > 0) warp_products<VALUES, V>(E, nent, 0, P, b_col, b_val, op);
+    __syncwarp();
+    if (stop && __shfl_sync(SG_FULL, *stop, 0)) return;
+  }
+}
+
+// Whole row with the whole block; chunks of blockDim A entries; every warp
+// takes a contiguous product range of each chunk.  `stop` (shared) aborts
+// between chunks.
+template <bool VALUES, typename V, class Op>
+__device__ __forceinline__ void block_row(int64_t row, const int64_t* __restrict__ a_ptr,
+                                          const int32_t* __restrict__ a_col, const V* __restrict__ a_val,
+                                          const int64_t* __restrict__ b_ptr, const int32_t* __restrict__ b_col,
+                                          const V* __restrict__ b_val, Entries E, int64_t* scan_scratch,
+                                          Op& op, volatile int* stop) {
+  const int nw = blockDim.x >> 5, w = warp_id();
+  const int64_t t1 = a_ptr[row + 1];
+  for (int64_t t = a_ptr[row]; t < t1; t += blockDim.x) {
+    int64_t bs = 0, len = 0;
+    double av = 0.0;
+    if (t + threadIdx.x < t1) {
+      const int32_t k = a_col[t + threadIdx.x];
+      bs = b_ptr[k];
+      len = b_ptr[k + 1] - bs;
+      if (VALUES) av = (double)a_val[t + threadIdx.x];
+    }
+    int64_t P, nent64;
+    const int64_t S = block_excl_scan(len, scan_scratch, &P);
+    const int64_t pos = block_excl_scan((int64_t)(len > 0), scan_scratch, &nent64);
+    if (len > 0) {
+      E.S[pos] = S;
+      E.bs[pos] = bs;
+      if (VALUES) E.av[pos] = av;
+    }
+    __syncthreads();
+    const int64_t per = ((P + nw - 1) / nw + 31) & ~(int64_t)31;
+    const int64_t pb = min(P, per * w), pe = min(P, per * (w + 1));
+    warp_products<VALUES, V>(E, (int)nent64, pb, pe, b_col, b_val, op);
+    __syncthreads();
+    if (stop && *stop) return;
+  }
+}
+
+struct WarpSync {
+  __device__ __forceinline__ void operator()() const { __syncwarp(); }
+};
+struct BlockSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+// -------------------------------------------------------------------------
+// row limit (reference overflow rule) and output type helpers
+
+__device__ __forceinline__ int64_t row_limit(const int8_t* kind, const int64_t* cap, const int64_t* alloc,
+                                             int64_t row) {
+  if (!kind) return NOLIMIT;
+  const int8_t k = kind[row];
+  if (k == SG_KIND_HASH || k == SG_KIND_ENHANCED_HASH) return (int64_t)(0.8 * (double)cap[row]);
+  if (k == SG_KIND_DENSE) return alloc[row];
+  return NOLIMIT;
+}
+
+// bitonic sort of n = pow2 (key, val) pairs in shared memory by a group of
+// `gsize` threads starting at thread `gtid`; `sync` is a group barrier.
+template <class Sync>
+__device__ __forceinline__ void bitonic_kv(int* keys, double* vals, int n, int gtid, int gsize, Sync sync) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int q = gtid; q < (n >> 1); q += gsize) {
+        const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+        const int ixj = i | j;
+        const int ki = keys[i], kj = keys[ixj];
+        const bool up = (i & k) == 0;
+        if ((ki > kj) == up) {
+          keys[i] = kj;
+          keys[ixj] = ki;
+          if (vals) {
+            const double t = vals[i];
+            vals[i] = vals[ixj];
+            vals[ixj] = t;
+          }
+        }
+      }
+      sync();
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
+// HW: warp-per-row shared-memory hash
+
+constexpr int HW_WARPS = 4;
+
+template <int MODE>
+struct HashOp {
+  int* keys;
+  double* vals;
+  int* cnt;
+  int* ovf;
+  int log2t;
+  int64_t limit;
+  __device__ __forceinline__ void operator()(int32_t col, double v) {
+    const int T = 1 << log2t;
+    uint32_t s = slot_hash((uint32_t)col, log2t);
+    volatile int* vk = keys;
+    for (int probe = 0; probe < T; ++probe) {
+      int k = vk[s];
+      if (k == col) {
+        if (MODE) smem_add(&vals[s], v);
+        return;
+      }
+      if (k == -1) {
+        const int old = atomicCAS(&keys[s], -1, col);
+        if (old == -1) {
+          const int c = atomicAdd(cnt, 1);
+          if ((int64_t)c >= limit) *ovf = 1;
+          if (MODE) smem_add(&vals[s], v);
+          return;
+        }
+        if (old == col) {
+          if (MODE) smem_add(&vals[s], v);
+          return;
+        }
+      }
+      s = (s + 1) & (T - 1);
+    }
+    *ovf = 1;
+  }
+};
+
+template <int LOG2T, int MODE, typename V>
+__global__ void __launch_bounds__(HW_WARPS * 32) k_hash_warp(int64_t nbin, const int32_t* __restrict__ rows,
+                                                             Csr A, Csr B, const int8_t* kind, const int64_t* cap,
+                                                             const int64_t* alloc, const int64_t* __restrict__ out_off,
+                                                             int32_t* __restrict__ out_col, V* __restrict__ out_val,
+                                                             int64_t* __restrict__ counts,
+                                                             uint8_t* __restrict__ overflow) {
+  constexpr int T = 1 << LOG2T;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int w = warp_id(), lane = lane_id();
+  // per-warp layout: S[33] bs[33] av[33] (int64/double), keys[T], vals[T], cnt, ovf
+  constexpr size_t ENT = 3 * 33 * 8;
+  constexpr size_t PER = ENT + (size_t)T * 4 + (MODE ? (size_t)T * 8 : 0) + 16;
+  unsigned char* base = smem + (size_t)w * ((PER + 15) & ~size_t(15));
+  Entries E{reinterpret_cast<int64_t*>(base), reinterpret_cast<int64_t*>(base) + 33,
+            reinterpret_cast<double*>(base) + 66};
+  double* vals = reinterpret_cast<double*>(base + ENT);
+  int* keys = reinterpret_cast<int*>(base + ENT + (MODE ? (size_t)T * 8 : 0));
+  int* cnt = keys + T;
+  int* ovf = cnt + 1;
+  const int64_t wid = (int64_t)blockIdx.x * HW_WARPS + w;
+  if (wid >= nbin) return;
+  const int64_t row = rows[wid];
+  for (int i = lane; i < T; i += 32) {
+    keys[i] = -1;
+    if (MODE) vals[i] = 0.0;
+  }
+  if (lane == 0) {
+    *cnt = 0;
+    *ovf = 0;
+  }
+  __syncwarp();
+  HashOp<MODE> op{keys, vals, cnt, ovf, LOG2T, row_limit(kind, cap, alloc, row)};
+  warp_row<MODE == 1, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, op,
+                         MODE ? ovf : nullptr);
+  __syncwarp();
+  if (MODE == 0) {
+    if (lane == 0) counts[row] = *cnt;
+    return;
+  }
+  if (*ovf) {
+    if (lane == 0) {
+      counts[row] = 0;
+      overflow[row] = 1;
+    }
+    return;
+  }
+  // compact occupied slots to the front, in slot order, in place
+  int n = 0;
+  for (int s0 = 0; s0 < T; s0 += 32) {
+    const int k = keys[s0 + lane];
+    const double v = vals[s0 + lane];
+    const bool occ = k != -1;
+    const unsigned b = __ballot_sync(SG_FULL, occ);
+    __syncwarp();
+    if (occ) {
+      const int pos = n + __popc(b & lanemask_lt());
+      keys[pos] = k;
+      vals[pos] = v;
+    }
+    n += __popc(b);
+    __syncwarp();
+  }
+  const int pad = (int)next_pow2_u32((uint32_t)max(n, 1));
+  for (int i = n + lane; i < pad; i += 32) keys[i] = INT_MAX;
+  __syncwarp();
+  bitonic_kv(keys, vals, pad, lane, 32, WarpSync{});
+  const int64_t off = out_off[row];
+  for (int i = lane; i < n; i += 32) {
+    out_col[off + i] = keys[i];
+    out_val[off + i] = (V)vals[i];
+  }
+  if (lane == 0) {
+    counts[row] = n;
+    overflow[row] = 0;
+  }
+}
+
+template <int LOG2T, int MODE>
+constexpr size_t hw_smem() {
+  return (size_t)HW_WARPS * (((3 * 33 * 8 + ((size_t)1 << LOG2T) * 4 + (MODE ? ((size_t)1 << LOG2T) * 8 : 0) + 16) + 15) &
+                             ~size_t(15));
+}
+
+// -------------------------------------------------------------------------
+// HB: block-per-row shared-memory hash
+
+template <int LOG2T, int MODE, typename V, int NT>
+__global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* __restrict__ rows, Csr A, Csr B,
+                                                   const int8_t* kind, const int64_t* cap, const int64_t* alloc,
+                                                   const int64_t* __restrict__ out_off,
+                                                   int32_t* __restrict__ out_col, V* __restrict__ out_val,
+                                                   int64_t* __restrict__ counts, uint8_t* __restrict__ overflow) {
+  constexpr int T = 1 << LOG2T;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int64_t scr[NT / 32 + 2];
+  __shared__ int cnt, ovf;
+  double* vals = reinterpret_cast<double*>(smem);
+  int* keys = reinterpret_cast<int*>(smem + (MODE ? (size_t)T * 8 : 0));
+  unsigned char* ebase = smem + (MODE ? (size_t)T * 8 : 0) + (size_t)T * 4;
+  Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (NT + 1),
+            reinterpret_cast<double*>(ebase) + 2 * (NT + 1)};
+  for (int64_t b = blockIdx.x; b < nbin; b += gridDim.x) {
+    const int64_t row = rows[b];
+    for (int i = threadIdx.x; i < T; i += NT) {
+      keys[i] = -1;
+      if (MODE) vals[i] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+      cnt = 0;
+      ovf = 0;
+    }
+    __syncthreads();
+    HashOp<MODE> op{keys, vals, &cnt, &ovf, LOG2T, row_limit(kind, cap, alloc, row)};
+    block_row<MODE == 1, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, op,
+                            MODE ? &ovf : nullptr);
+    __syncthreads();
+    if (MODE == 0) {
+      if (threadIdx.x == 0) counts[row] = cnt;
+      __syncthreads();
+      continue;
+    }
+    if (ovf) {
+      if (threadIdx.x == 0) {
+        counts[row] = 0;
+        overflow[row] = 1;
+      }
+      __syncthreads();
+      continue;
+    }
+    // in-place ordered compaction, chunks of NT slots
+    int64_t n = 0;
+    for (int s0 = 0; s0 < T; s0 += NT) {
+      const int k = keys[s0 + threadIdx.x];
+      const double v = vals[s0 + threadIdx.x];
+      int64_t tot;
+      const int64_t pos = block_excl_scan((int64_t)(k != -1), scr, &tot);
+      if (k != -1) {
+        keys[n + pos] = k;
+        vals[n + pos] = v;
+      }
+      n += tot;
+      __syncthreads();
+    }
+    const int pad = (int)next_pow2_u32((uint32_t)max((int)n, 1));
+    for (int i = (int)n + threadIdx.x; i < pad; i += NT) keys[i] = INT_MAX;
+    __syncthreads();
+    bitonic_kv(keys, vals, pad, threadIdx.x, NT, BlockSync{});
+    const int64_t off = out_off[row];
+    for (int i = threadIdx.x; i < n; i += NT) {
+      out_col[off + i] = keys[i];
+      out_val[off + i] = (V)vals[i];
+    }
+    if (threadIdx.x == 0) {
+      counts[row] = n;
+      overflow[row] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+template <int LOG2T, int MODE, int NT>
+constexpr size_t hb_smem() {
+  return ((size_t)1 << LOG2T) * (MODE ? 12 : 4) + (size_t)3 * (NT + 1) * 8;
+}
+
+// -------------------------------------------------------------------------
+// ESC: warp per row, <= 64 products (accumulate.py:254-271, 368-378)
+
+constexpr int ESC_WARPS = 8;
+
+
+template <typename V>
+__global__ void __launch_bounds__(ESC_WARPS * 32) k_esc(int64_t nbin, const int32_t* __restrict__ rows, Csr A, Csr B,
+                                                        const int64_t* __restrict__ out_off,
+                                                        int32_t* __restrict__ out_col, V* __restrict__ out_val,
+                                                        int64_t* __restrict__ counts, uint8_t* __restrict__ overflow) {
+  __shared__ int64_t ent[ESC_WARPS][3 * 33];
+  __shared__ unsigned long long key[ESC_WARPS][64];
+  __shared__ double val[ESC_WARPS][64];
+  __shared__ double vsorted[ESC_WARPS][64];
+  const int w = warp_id(), lane = lane_id();
+  const int64_t wid = (int64_t)blockIdx.x * ESC_WARPS + w;
+  if (wid >= nbin) return;
+  const int64_t row = rows[wid];
+  Entries E{ent[w], ent[w] + 33, reinterpret_cast<double*>(ent[w] + 66)};
+  // gather products in stream order
+  int np = 0;
+  const int64_t t1 = A.ptr[row + 1];
+  for (int64_t t = A.ptr[row]; t < t1; t += 32) {
+    int nent;
+    const int64_t P = warp_load_chunk<true, V>(t, t1, A.col, (const V*)A.val, B.ptr, E, nent);
+    for (int64_t p0 = 0; p0 < P; p0 += 32) {
+      // owner search (small chunks: linear)
+      const int64_t p = p0 + lane;
+      if (p < P) {
+        int c = 0;
+        while (c + 1 < nent && E.S[c + 1] <= p) ++c;
+        const int64_t j = E.bs[c] + (p - E.S[c]);
+        const int pos = np + (int)p;
+        if (pos < 64) {
+          key[w][pos] = ((unsigned long long)(uint32_t)B.col[j] << 32) | (unsigned)pos;
+          val[w][pos] = E.av[c] * (double)((const V*)B.val)[j];
+        }
+      }
+    }
+    np += (int)P;
+    __syncwarp();
+  }
+  np = min(np, 64);
+  for (int i = np + lane; i < 64; i += 32) key[w][i] = ~0ull;
+  __syncwarp();
+  // bitonic sort of 64 packed (col, product index) keys: stable by construction
+  for (int k = 2; k <= 64; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int q = lane;  // 32 pairs
+      const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+      const int ixj = i | j;
+      const unsigned long long ki = key[w][i], kj = key[w][ixj];
+      const bool up = (i & k) == 0;
+      if ((ki > kj) == up) {
+        key[w][i] = kj;
+        key[w][ixj] = ki;
+      }
+      __syncwarp();
+    }
+  for (int i = lane; i < np; i += 32) vsorted[w][i] = val[w][(unsigned)(key[w][i] & 0xffffffffu)];
+  __syncwarp();
+  // heads and segmented sums (sequential within a run, stream order)
+  int nhead = 0;
+  const int64_t off = out_off[row];
+  for (int base = 0; base < np; base += 32) {
+    const int i = base + lane;
+    bool head = false;
+    if (i < np) head = (i == 0) || ((key[w][i] >> 32) != (key[w][i - 1] >> 32));
+    const unsigned hb = __ballot_sync(SG_FULL, head);
+    if (head) {
+      double s = vsorted[w][i];
+      for (int r = i + 1; r < np && (key[w][r] >> 32) == (key[w][i] >> 32); ++r) s += vsorted[w][r];
+      const int pos = nhead + __popc(hb & lanemask_lt());
+      out_col[off + pos] = (int32_t)(key[w][i] >> 32);
+      out_val[off + pos] = (V)s;
+    }
+    nhead += __popc(hb);
+  }
+  if (lane == 0) {
+    counts[row] = nhead;
+    overflow[row] = 0;
+  }
+}
+
+// -------------------------------------------------------------------------
+// BM: block-per-row bitmap over the column span (windows of BW*64 columns)
+
+template <typename V>
+struct BitmapSetOp {
+  unsigned long long* bm;
+  int64_t wlo, whi;
+  __device__ __forceinline__ void operator()(int32_t col, double) {
+    if (col < wlo || col > whi) return;
+    const int64_t x = col - wlo;
+    // 32-bit ATOMS.OR is native on sm_100a (the 64-bit form is a CAS loop)
+    atomicOr(reinterpret_cast<unsigned*>(bm) + (x >> 5), 1u << (x & 31));
+  }
+};
+
+template <typename V>
+struct BitmapAddOp {
+  const unsigned long long* bm;
+  const int* pre;
+  int64_t wlo, whi;
+  V* out;  // already offset to the window's first output slot
+  __device__ __forceinline__ void operator()(int32_t col, double v) {
+    if (col < wlo || col > whi) return;
+    const int64_t x = col - wlo;
+    const int w = (int)(x >> 6);
+    const unsigned long long below = bm[w] & ((1ull << (x & 63)) - 1ull);
+    gmem_red(out + pre[w] + __popcll(below), (V)v);
+  }
+};
+
+template <int BW, int MODE, typename V, int NT>
+__global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __restrict__ rows, Csr A, Csr B,
+                                               const int8_t* kind, const int64_t* cap, const int64_t* alloc,
+                                               const int64_t* __restrict__ span_lo,
+                                               const int64_t* __restrict__ span_hi,
+                                               const int64_t* __restrict__ out_off,
+                                               int32_t* __restrict__ out_col, V* __restrict__ out_val,
+                                               int64_t* __restrict__ counts, uint8_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int64_t scr[NT / 32 + 2];
+  unsigned long long* bm = reinterpret_cast<unsigned long long*>(smem);
+  int* pre = reinterpret_cast<int*>(smem + (size_t)BW * 8);
+  unsigned char* ebase = smem + (size_t)BW * 12;
+  Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (NT + 1),
+            reinterpret_cast<double*>(ebase) + 2 * (NT + 1)};
+  constexpr int64_t WCOLS = (int64_t)BW * 64;
+  constexpr int WPT = (BW + NT - 1) / NT;  // words per thread
+  for (int64_t b = blockIdx.x; b < nbin; b += gridDim.x) {
+    const int64_t row = rows[b];
+    const int64_t lo = span_lo[row], hi = span_hi[row];
+    const int64_t limit = row_limit(kind, cap, alloc, row);
+    int64_t total = 0;
+    const bool multi = hi - lo + 1 > WCOLS;
+    // count-only sweep first when a limit applies and the span needs windows
+    bool over = false;
+    if (MODE == 1 && limit != NOLIMIT && multi) {
+      for (int64_t wlo = lo; wlo <= hi; wlo += WCOLS) {
+        const int64_t whi = min(hi, wlo + WCOLS - 1);
+        const int nwords = (int)((whi - wlo) / 64 + 1);
+        for (int i = threadIdx.x; i < nwords; i += NT) bm[i] = 0ull;
+        __syncthreads();
+        BitmapSetOp<V> so{bm, wlo, whi};
+        block_row<false, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, so,
+                            nullptr);
+        int64_t c = 0;
+        for (int i = threadIdx.x; i < nwords; i += NT) c += __popcll(bm[i]);
+        int64_t tot;
+        block_excl_scan(c, scr, &tot);
+        total += tot;
+      }
+      over = total > limit;
+      total = 0;
+    }
+    if (over) {
+      if (threadIdx.x == 0) {
+        counts[row] = 0;
+        if (overflow) overflow[row] = 1;
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int64_t wlo = lo; wlo <= hi; wlo += WCOLS) {
+      const int64_t whi = min(hi, wlo + WCOLS - 1);
+      const int nwords = (int)((whi - wlo) / 64 + 1);
+      for (int i = threadIdx.x; i < nwords; i += NT) bm[i] = 0ull;
+      __syncthreads();
+      BitmapSetOp<V> so{bm, wlo, whi};
+      block_row<false, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, so, nullptr);
+      // per-thread contiguous words -> exclusive prefix of popcounts
+      int64_t c = 0;
+      const int w0 = threadIdx.x * WPT;
+#pragma unroll 4
+      for (int i = 0; i < WPT; ++i)
+        if (w0 + i < nwords) c += __popcll(bm[w0 + i]);
+      int64_t wtot;
+      int64_t run = block_excl_scan(c, scr, &wtot);
+      if (MODE == 0) {
+        total += wtot;
+        continue;
+      }
+      if (!multi && total + wtot > limit) {
+        over = true;
+        break;
+      }
+      for (int i = 0; i < WPT; ++i)
+        if (w0 + i < nwords) {
+          pre[w0 + i] = (int)run;
+          run += __popcll(bm[w0 + i]);
+        }
+      __syncthreads();
+      const int64_t base = out_off[row] + total;
+      // emit sorted columns from the bitmap and clear the value slots
+      for (int i = threadIdx.x; i < nwords; i += NT) {
+        unsigned long long bits = bm[i];
+        int64_t pos = base + pre[i];
+        while (bits) {
+          const int bb = __ffsll((long long)bits) - 1;
+          bits &= bits - 1;
+          out_col[pos++] = (int32_t)(wlo + (int64_t)i * 64 + bb);
+        }
+      }
+      for (int64_t i = threadIdx.x; i < wtot; i += NT) out_val[base + i] = (V)0;
+      __syncthreads();
+      BitmapAddOp<V> ao{bm, pre, wlo, whi, out_val + base};
+      block_row<true, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, ao, nullptr);
+      total += wtot;
+    }
+    if (threadIdx.x == 0) {
+      if (MODE == 0) {
+        counts[row] = total;
+      } else {
+        counts[row] = over ? 0 : total;
+        if (overflow) overflow[row] = over ? 1 : 0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int BW, int NT>
+constexpr size_t bm_smem() {
+  return (size_t)BW * 12 + (size_t)3 * (NT + 1) * 8;
+}
+
+// -------------------------------------------------------------------------
+// classification
+
+// bin ids shared by all modes
+enum Bin : uint8_t {
+  BIN_NONE = 0,
+  BIN_ESC = 1,
+  BIN_HW0 = 2,  // T = 32 << (bin - BIN_HW0), up to 2048 (bins 2..8)
+  BIN_HB0 = 9,  // T = 4096 << (bin - BIN_HB0), up to 32768 (bins 9..12); numeric uses 2048..16384 via HB_N0
+  BIN_BM0 = 13, // BW = 256, 2048, 16384 (bins 13..15)
+  BIN_HBN = 16, // numeric HB T = 2048 (bin 16)
+  NBINS = 17
+};
+
+__device__ __forceinline__ uint8_t bm_bin(int64_t span) {
+  const int64_t words = (span + 63) / 64;
+  if (words <= 256) return BIN_BM0;
+  if (words <= 2048) return BIN_BM0 + 1;
+  return BIN_BM0 + 2;
+}
+
+__device__ __forceinline__ int log2_pow2(int64_t t) { return 63 - __clzll((unsigned long long)t); }
+
+__device__ __forceinline__ int64_t pow2_at_least(int64_t x) {
+  return x <= 1 ? 1 : (int64_t)1 << (64 - __clzll((unsigned long long)(x - 1)));
+}
+
+// mode 0 (symbolic)
+__global__ void k_classify_count(int64_t m, const int64_t* __restrict__ products, const int64_t* __restrict__ lo,
+                                 const int64_t* __restrict__ hi, uint8_t* __restrict__ bins,
+                                 int64_t* __restrict__ counts) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int64_t p = products[i];
+  uint8_t b;
+  if (p == 0) {
+    b = BIN_NONE;
+    counts[i] = 0;
+  } else {
+    const int64_t span = hi[i] - lo[i] + 1;
+    const int64_t T = max(pow2_at_least(2 * p), (int64_t)32);
+    if (p <= 1024) {
+      b = (uint8_t)(BIN_HW0 + log2_pow2(T) - 5);
+    } else if (span <= ((int64_t)1 << 20) && (span + 63) / 64 <= p) {
+      b = bm_bin(span);
+    } else if (T <= 32768) {
+      b = (uint8_t)(BIN_HB0 + log2_pow2(max(T, (int64_t)4096)) - 12);
+    } else {
+      b = bm_bin(span);
+    }
+  }
+  bins[i] = b;
+}
+
+// mode 1 (numeric phase)
+__global__ void k_classify_numeric(int64_t m, const int8_t* __restrict__ kind, const int64_t* __restrict__ cap,
+                                   const int64_t* __restrict__ alloc, const int64_t* __restrict__ products,
+                                   const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
+                                   uint8_t* __restrict__ bins, int64_t* __restrict__ counts,
+                                   uint8_t* __restrict__ overflow) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int64_t p = products[i];
+  const int8_t k = kind[i];
+  uint8_t b;
+  if (p == 0 || k == SG_KIND_FALLBACK) {
+    b = BIN_NONE;
+    counts[i] = 0;
+    overflow[i] = 0;
+  } else {
+    const int64_t span = hi[i] - lo[i] + 1;
+    const int64_t limit = row_limit(kind, cap, alloc, i);
+    if (k == SG_KIND_ESC && p <= 64) {
+      b = BIN_ESC;
+    } else if (k == SG_KIND_DENSE) {
+      b = bm_bin(span);
+    } else {
+      const int64_t need = min(limit == NOLIMIT ? p : limit + 1, p);
+      const int64_t T = max(pow2_at_least(2 * need), (int64_t)32);
+      if (T <= 1024 && p <= 4096)
+        b = (uint8_t)(BIN_HW0 + log2_pow2(T) - 5);
+      else if (T <= 2048)
+        b = BIN_HBN;
+      else if (T <= 16384)
+        b = (uint8_t)(BIN_HB0 + log2_pow2(T) - 12);
+      else
+        b = bm_bin(span);
+    }
+  }
+  bins[i] = b;
+}
+
+// fallback rows: bitmap family by span
+__global__ void k_classify_fallback(int64_t nrows, const int64_t* __restrict__ rows, const int64_t* __restrict__ lo,
+                                    const int64_t* __restrict__ hi, uint8_t* __restrict__ bins) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  const int64_t r = rows[i];
+  bins[i] = bm_bin(hi[r] - lo[r] + 1);
+}
+
+// -------------------------------------------------------------------------
+// launch helpers
+
+template <class K>
+static int set_smem(K kern, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) {
+      set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      return SG_ERR_CUDA;
+    }
+  }
+  return SG_OK;
+}
+
+static int num_sms() {
+  static int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  return sms;
+}
+
+struct Launch {
+  Csr A, B;
+  const int8_t* kind;
+  const int64_t* cap;
+  const int64_t* alloc;
+  const int64_t* lo;
+  const int64_t* hi;
+  const int64_t* out_off;
+  int32_t* out_col;
+  void* out_val;
+  int64_t* counts;
+  uint8_t* overflow;
+  cudaStream_t s;
+};
+
+template <int LOG2T, int MODE, typename V>
+static int launch_hw(const Launch& L, const int32_t* rows, int64_t n) {
+  constexpr size_t sm = hw_smem<LOG2T, MODE>();
+  auto kern = k_hash_warp<LOG2T, MODE, V>;
+  if (int rc = set_smem(kern, sm)) return rc;
+  kern<<<grid_for(n, HW_WARPS), HW_WARPS * 32, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.out_off,
+                                                         L.out_col, (V*)L.out_val, L.counts, L.overflow);
+  return check_cuda("k_hash_warp");
+}
+
+template <int LOG2T, int MODE, typename V, int NT>
+static int launch_hb(const Launch& L, const int32_t* rows, int64_t n) {
+  constexpr size_t sm = hb_smem<LOG2T, MODE, NT>();
+  auto kern = k_hash_block<LOG2T, MODE, V, NT>;
+  if (int rc = set_smem(kern, sm)) return rc;
+  int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 16);
+  kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.out_off, L.out_col, (V*)L.out_val,
+                           L.counts, L.overflow);
+  return check_cuda("k_hash_block");
+}
+
+template <int BW, int MODE, typename V, int NT>
+static int launch_bm(const Launch& L, const int32_t* rows, int64_t n) {
+  constexpr size_t sm = bm_smem<BW, NT>();
+  auto kern = k_bitmap<BW, MODE, V, NT>;
+  if (int rc = set_smem(kern, sm)) return rc;
+  int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 32);
+  kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.lo, L.hi, L.out_off, L.out_col,
+                           (V*)L.out_val, L.counts, L.overflow);
+  return check_cuda("k_bitmap");
+}
+
+template <int MODE, typename V>
+static int launch_bin(int bin, const Launch& L, const int32_t* rows, int64_t n) {
+  if (n == 0) return SG_OK;
+  switch (bin) {
+    case BIN_ESC:
+      if (MODE == 1) {
+        k_esc<V><<<grid_for(n, ESC_WARPS), ESC_WARPS * 32, 0, L.s>>>(n, rows, L.A, L.B, L.out_off, L.out_col,
+                                                                     (V*)L.out_val, L.counts, L.overflow);
+        return check_cuda("k_esc");
+      }
+      return SG_ERR_ARG;
+    case BIN_HW0 + 0: return launch_hw<5, MODE, V>(L, rows, n);
+    case BIN_HW0 + 1: return launch_hw<6, MODE, V>(L, rows, n);
+    case BIN_HW0 + 2: return launch_hw<7, MODE, V>(L, rows, n);
+    case BIN_HW0 + 3: return launch_hw<8, MODE, V>(L, rows, n);
+    case BIN_HW0 + 4: return launch_hw<9, MODE, V>(L, rows, n);
+    case BIN_HW0 + 5: return launch_hw<10, MODE, V>(L, rows, n);
+    case BIN_HW0 + 6:
+      if (MODE == 0) return launch_hw<11, 0, V>(L, rows, n);
+      return SG_ERR_ARG;
+    case BIN_HBN: return launch_hb<11, MODE, V, 256>(L, rows, n);
+    case BIN_HB0 + 0: return launch_hb<12, MODE, V, 512>(L, rows, n);
+    case BIN_HB0 + 1: return launch_hb<13, MODE, V, 512>(L, rows, n);
+    case BIN_HB0 + 2: return launch_hb<14, MODE, V, 512>(L, rows, n);
+    case BIN_HB0 + 3:
+      if (MODE == 0) return launch_hb<15, 0, V, 512>(L, rows, n);
+      return SG_ERR_ARG;
+    case BIN_BM0 + 0: return launch_bm<256, MODE, V, 256>(L, rows, n);
+    case BIN_BM0 + 1: return launch_bm<2048, MODE, V, 256>(L, rows, n);
+    case BIN_BM0 + 2: return launch_bm<16384, MODE, V, 1024>(L, rows, n);
+  }
+  set_error("launch_bin: unexpected bin " + std::to_string(bin));
+  return SG_ERR_ARG;
+}
+
+// bins in launch order: heaviest families first so they start early
+static const int kOrder[] = {BIN_BM0 + 2, BIN_HB0 + 3, BIN_HB0 + 2, BIN_HB0 + 1, BIN_HB0 + 0, BIN_BM0 + 1,
+                             BIN_HBN,     BIN_BM0 + 0, BIN_HW0 + 6, BIN_HW0 + 5, BIN_HW0 + 4, BIN_HW0 + 3,
+                             BIN_HW0 + 2, BIN_HW0 + 1, BIN_HW0 + 0, BIN_ESC};
+
+template <int MODE, typename V>
+static int run_bins(const Launch& L, int64_t m, Workspace& w, const int32_t* rowmap_unused) {
+  int64_t cnt[NBINS], off[NBINS + 1];
+  if (int rc = partition_rows(m, NBINS, w, cnt, off, L.s)) return rc;
+  for (int b : kOrder) {
+    if (cnt[b] == 0) continue;
+    if (int rc = launch_bin<MODE, V>(b, L, w.rowlist + off[b], cnt[b])) return rc;
+  }
+  return SG_OK;
+}
+
+// fallback rows are given as a list; map through it
+__global__ void k_gather_rows(int64_t n, const int32_t* __restrict__ idx, const int64_t* __restrict__ rows,
+                              int32_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (int32_t)rows[idx[i]];
+}
+
+}  // namespace sg
+
+using namespace sg;
+
+extern "C" {
+
+int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col, const int64_t* b_ptr,
+                const int32_t* b_col, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
+                int64_t* counts, void* ws, size_t ws_bytes, void* stream) {
+  Workspace w;
+  if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
+  if (m == 0) return SG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_classify_count<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, w.bins, counts);
+  if (int rc = check_cuda("k_classify_count")) return rc;
+  Launch L{{a_ptr, a_col, nullptr}, {b_ptr, b_col, nullptr}, nullptr, nullptr, nullptr, span_lo, span_hi,
+           nullptr, nullptr, nullptr, counts, nullptr, s};
+  (void)b_ncols;
+  return run_bins<0, double>(L, m, w, nullptr);
+}
+
+int sg_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, const int32_t* a_col,
+               const void* a_val, const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
+               const int8_t* kind, const int64_t* cap, const int64_t* alloc, const int64_t* products,
+               const int64_t* span_lo, const int64_t* span_hi, const int64_t* out_off, int32_t* out_col,
+               void* out_val, int64_t* counts, uint8_t* overflow, void* ws, size_t ws_bytes, void* stream) {
+  Workspace w;
+  if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
+  if (m == 0) return SG_OK;
+  (void)b_ncols;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_classify_numeric<<<grid_for(m, 256), 256, 0, s>>>(m, kind, cap, alloc, products, span_lo, span_hi, w.bins,
+                                                      counts, overflow);
+  if (int rc = check_cuda("k_classify_numeric")) return rc;
+  Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, kind, cap, alloc, span_lo, span_hi,
+           out_off, out_col, out_val, counts, overflow, s};
+  if (dtype == SG_F64) return run_bins<1, double>(L, m, w, nullptr);
+  if (dtype == SG_F32) return run_bins<1, float>(L, m, w, nullptr);
+  set_error("sg_numeric: bad dtype");
+  return SG_ERR_ARG;
+}
+
+int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, int dtype, const int64_t* a_ptr,
+                const int32_t* a_col, const void* a_val, const int64_t* b_ptr, const int32_t* b_col,
+                const void* b_val, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
+                const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts, void* ws,
+                size_t ws_bytes, void* stream) {
+  Workspace w;
+  if (!carve(ws, ws_bytes, nrows, w)) return SG_ERR_WORKSPACE;
+  if (nrows == 0) return SG_OK;
+  (void)b_ncols;
+  (void)products;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_classify_fallback<<<grid_for(nrows, 256), 256, 0, s>>>(nrows, rows, span_lo, span_hi, w.bins);
+  if (int rc = check_cuda("k_classify_fallback")) return rc;
+  int64_t cnt[NBINS], off[NBINS + 1];
+  if (int rc = partition_rows(nrows, NBINS, w, cnt, off, s)) return rc;
+  // rowlist holds indices into `rows`; translate to row ids in place via tmp
+  int32_t* mapped = reinterpret_cast<int32_t*>(w.tmp);
+  k_gather_rows<<<grid_for(nrows, 256), 256, 0, s>>>(nrows, w.rowlist, rows, mapped);
+  if (int rc = check_cuda("k_gather_rows")) return rc;
+  Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, nullptr, nullptr, nullptr, span_lo, span_hi,
+           out_off, out_col, out_val, counts, nullptr, s};
+  for (int b : kOrder) {
+    if (cnt[b] == 0) continue;
+    int rc;
+    if (mode == 0)
+      rc = launch_bin<0, double>(b, L, mapped + off[b], cnt[b]);
+    else if (dtype == SG_F64)
+      rc = launch_bin<1, double>(b, L, mapped + off[b], cnt[b]);
+    else
+      rc = launch_bin<1, float>(b, L, mapped + off[b], cnt[b]);
+    if (rc) return rc;
+  }
+  return SG_OK;
+}
+
+}  // extern "C"

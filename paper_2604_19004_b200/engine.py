@@ -1,0 +1,371 @@
+"""Drop-in ``spgemm(a, b, cfg, deadline) -> (C, RunReport)`` on one B200.
+
+Same stage sequence, decisions and report as the reference engine
+(``engine.py:136-249``): analysis -> [sketch + sampled CR] -> size prediction
+(symbolic | HLL estimate | upper bound) -> binning -> numeric -> fallback ->
+sort + compact.  Every stage runs as sm_100a kernels behind the C ABI
+(``include/sgb200.h``) through ctypes; torch is used only to allocate device
+buffers and to move bytes.  The only host arithmetic is what the reference's
+host does on scalars: workflow choice, the seeded sample-row draw and the
+10k-row sampled-CR reduction.
+
+Memory layout differences (results are identical):
+  * with an EXACT prediction (symbolic workflow) C is allocated once at its
+    final size and every kernel writes its rows in place, sorted: no staging
+    slab, no compaction copy;
+  * otherwise the main staging slab holds only rows that the numeric phase
+    accumulates (planned-FALLBACK rows are never staged, as their staged
+    region is unused in the reference too); fallback rows are counted first,
+    then written straight into C.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import (DEFAULT_SAMPLE_MAX, DEFAULT_SAMPLE_MIN, PRECISION_FOR, EngineConfig,
+                     PlanKind, ResourceLimitError, RunReport, TierConfig, WorkflowKind,
+                     WorkflowOverride, DeadlineExceeded, select_registers, select_workflow)
+from .csr import CsrMatrix
+from .device import DeviceCsr, to_device, ptr
+
+ALPHA = {32: 0.697, 64: 0.709, 128: 0.7213 / (1 + 1.079 / 128)}
+_PRED_CODE = {"exact": 0, "estimated": 1, "upper_bound": 2}
+
+
+def _check_deadline(deadline):
+    if deadline is not None and time.perf_counter() > deadline:
+        raise DeadlineExceeded("run exceeded its deadline")
+
+
+def lin_table(m: int) -> np.ndarray:
+    """m*ln(m/z) for z = 0..m (z = 0 unused), computed with the reference's
+    own array expression (hll.py:84) so the device linear-counting branch is
+    bit-identical."""
+    z = np.arange(0, m + 1)
+    with np.errstate(divide="ignore"):
+        t = np.where(z > 0, m * np.log(m / np.maximum(z, 1)), 0.0)
+    return t.astype(np.float64)
+
+
+def sample_rows(nrows: int, ratio: float, min_n: int, max_n: int, seed: int) -> np.ndarray:
+    """Seeded sample of distinct rows, identical draw to analysis.py:182-190."""
+    n = int(np.clip(round(ratio * nrows), min(min_n, nrows), min(max_n, nrows)))
+    if n >= nrows:
+        return np.arange(nrows, dtype=np.int64)
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(nrows, size=n, replace=False)).astype(np.int64)
+
+
+def tiers_struct(t: TierConfig) -> _lib.SgTiers:
+    s = _lib.SgTiers()
+    s.n_hash = len(t.hash_capacities)
+    s.n_dense = len(t.dense_spans)
+    for i, c in enumerate(t.hash_capacities):
+        s.hash_caps[i] = int(c)
+    for i, c in enumerate(t.dense_spans):
+        s.dense_spans[i] = int(c)
+    s.enh_cap = int(t.enhanced_hash_capacity)
+    s.esc_max = int(t.esc_max_products)
+    s.coef = float(t.expansion_coef)
+    return s
+
+
+class _Ctx:
+    """Per-call device context: stream, workspace, timing."""
+
+    def __init__(self, device, stream):
+        self.device = device
+        self.stream = stream
+        self.sp = stream.cuda_stream
+        self.ws = None
+        self.ws_bytes = 0
+
+    def workspace(self, m):
+        need = int(_lib.load().sg_workspace_bytes(int(m)))
+        if self.ws is None or self.ws_bytes < need:
+            self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+            self.ws_bytes = need
+        return ptr(self.ws), self.ws_bytes
+
+    def empty(self, n, dtype):
+        try:
+            return torch.empty(int(n), dtype=dtype, device=self.device)
+        except torch.OutOfMemoryError as exc:
+            raise ResourceLimitError(
+                f"device allocation of {int(n)} x {dtype} failed; the symbolic workflow "
+                "(workflow='symbolic') stages exact-sized rows") from exc
+
+    def sync(self):
+        self.stream.synchronize()
+
+
+def row_stats(ctx: _Ctx, A: DeviceCsr, B: DeviceCsr):
+    m = A.nrows
+    products = ctx.empty(m, torch.int64)
+    lo = ctx.empty(m, torch.int64)
+    hi = ctx.empty(m, torch.int64)
+    totals = ctx.empty(2, torch.int64)
+    _lib.call("sg_row_stats", m, B.ncols, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr),
+              ptr(B.col_idx), ptr(products), ptr(lo), ptr(hi), ptr(totals), ctx.sp)
+    return products, lo, hi, totals
+
+
+def hll_build(ctx: _Ctx, B: DeviceCsr, p: int):
+    regs = ctx.empty(B.nrows * (1 << p), torch.uint8)
+    _lib.call("sg_hll_build", B.nrows, ptr(B.row_ptr), ptr(B.col_idx), p, ptr(regs), ctx.sp)
+    return regs
+
+
+def hll_estimate(ctx: _Ctx, A: DeviceCsr, regs, p: int, rows=None):
+    m = 1 << p
+    lin = torch.from_numpy(lin_table(m)).to(ctx.device)
+    nsel = A.nrows if rows is None else int(rows.numel())
+    est = ctx.empty(nsel, torch.float64)
+    _lib.call("sg_hll_estimate", nsel, None if rows is None else ptr(rows), ptr(A.row_ptr),
+              ptr(A.col_idx), ptr(regs), p, ptr(lin), (ALPHA[m] * m) * m, ptr(est), ctx.sp)
+    return est
+
+
+def scan(ctx: _Ctx, x):
+    n = int(x.numel())
+    out = ctx.empty(n + 1, torch.int64)
+    ws, wsb = ctx.workspace(max(n, 1))
+    _lib.call("sg_scan", n, ptr(x), ptr(out), ws, wsb, ctx.sp)
+    return out
+
+
+def _dtype_code(v: torch.Tensor) -> int:
+    return 0 if v.dtype == torch.float64 else 1
+
+
+def spgemm(a, b, cfg: EngineConfig | None = None, deadline: float | None = None):
+    """Multiply two CSR matrices on the GPU; returns (C, RunReport).
+
+    ``a`` / ``b`` are host ``CsrMatrix`` (any object with nrows, ncols,
+    row_ptr, col_idx, values) or ``DeviceCsr``.  C is a host ``CsrMatrix``
+    unless ``cfg.return_device``.  Raises ValueError on a dimension mismatch
+    (engine.py:145-146), ResourceLimitError when the reference staging rule
+    exceeds ``staging_limit_bytes`` (engine.py:259-271), DeadlineExceeded
+    between stages (engine.py:131-133).
+    """
+    cfg = cfg or EngineConfig()
+    if a.ncols != b.nrows:
+        raise ValueError(f"dimension mismatch: A is {a.nrows}x{a.ncols}, B is {b.nrows}x{b.ncols}")
+    _lib.load()
+    if not torch.cuda.is_available():
+        from .config import CudaLibraryError
+        raise CudaLibraryError("no CUDA device: the B200 path has no CPU fallback")
+    device = torch.device("cuda", cfg.device if cfg.device is not None else torch.cuda.current_device())
+    stream = cfg.stream if cfg.stream is not None else torch.cuda.current_stream(device)
+    with torch.cuda.device(device), torch.cuda.stream(stream):
+        return _spgemm(a, b, cfg, deadline, _Ctx(device, stream))
+
+
+def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
+    dtype = torch.float64
+    if cfg.dtype == "f32" or (cfg.dtype is None and np.dtype(getattr(a.values, "dtype", np.float64)) == np.float32
+                              and not isinstance(a, DeviceCsr)):
+        dtype = torch.float32
+    if isinstance(a, DeviceCsr) and cfg.dtype is None:
+        dtype = a.values.dtype
+    kms = {}
+    t0 = time.perf_counter()
+    A = to_device(a, ctx.device, dtype)
+    B = A if b is a else to_device(b, ctx.device, dtype)
+    m, n = A.nrows, B.ncols
+    kms["h2d"] = (time.perf_counter() - t0) * 1e3
+
+    # ---- analysis (analysis.py:96-128)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+    ev[0].record(ctx.stream)
+    t0 = time.perf_counter()
+    products, span_lo, span_hi, totals = row_stats(ctx, A, B)
+    tot = totals.cpu().numpy()
+    total_products = int(tot[0])
+    nnz_a = A.nnz
+    er = total_products / nnz_a if nnz_a else 0.0
+    avg = total_products / m if m else 0.0
+    ev[1].record(ctx.stream)
+    t1 = time.perf_counter()
+    _check_deadline(deadline)
+
+    # ---- sketch + sampled CR (engine.py:157-174)
+    registers = cfg.registers if cfg.registers is not None else select_registers(er)
+    p = PRECISION_FOR[registers]
+    regs = None
+    cr = None
+    W = cfg.workflow
+    if W is WorkflowOverride.FORCE_SYMBOLIC:
+        kind_wf = WorkflowKind.SYMBOLIC
+    elif W is WorkflowOverride.FORCE_UPPER_BOUND:
+        kind_wf = WorkflowKind.UPPER_BOUND
+    elif W is WorkflowOverride.AUTO and avg < 64:
+        kind_wf = WorkflowKind.UPPER_BOUND
+    else:
+        regs = hll_build(ctx, B, p)
+        if m == 0:
+            cr = (1.0, 1.0, 0.0)
+        else:
+            rows_h = sample_rows(m, cfg.sample_ratio, cfg.sample_min, cfg.sample_max, cfg.seed)
+            rows_d = torch.from_numpy(rows_h).to(ctx.device)
+            est_s = hll_estimate(ctx, A, regs, p, rows_d).cpu().numpy()
+            prods = products[rows_d].cpu().numpy().astype(np.float64)
+            cr_hat = float(prods.sum() / max(1.0, est_s.sum()))
+            row_cr = np.where(prods > 0, prods / np.maximum(est_s, 1.0), 1.0)
+            cr = (cr_hat, float(row_cr.mean()), float(row_cr.std()))
+        if W is WorkflowOverride.FORCE_ESTIMATE:
+            kind_wf = WorkflowKind.HLL_ESTIMATION
+        else:
+            kind_wf = select_workflow(avg, er, cr[0])
+    ev[2].record(ctx.stream)
+    ctx.sync()
+    t2 = time.perf_counter()
+    _check_deadline(deadline)
+
+    # ---- size prediction (predict.py)
+    ws, wsb = ctx.workspace(max(m, 1))
+    if kind_wf is WorkflowKind.SYMBOLIC:
+        pred = ctx.empty(m, torch.int64)
+        _lib.call("sg_symbolic", m, n, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
+                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(pred), ws, wsb, ctx.sp)
+        pred_kind = "exact"
+    elif kind_wf is WorkflowKind.HLL_ESTIMATION:
+        pred = hll_estimate(ctx, A, regs, p)
+        pred_kind = "estimated"
+    else:
+        pred = products
+        pred_kind = "upper_bound"
+    ev[3].record(ctx.stream)
+    ctx.sync()
+    t3 = time.perf_counter()
+    _check_deadline(deadline)
+
+    # ---- binning (accumulate.plan_rows) + numeric phase (engine._numeric_phase)
+    coef = cfg.coef
+    if coef is None:
+        coef = 2.0 if registers == 32 else cfg.tiers.expansion_coef
+    tiers = replace(cfg.tiers, expansion_coef=coef)
+    bitmap_query = cr is not None and max(1.0, cr[1] - 2.0 * cr[2]) >= tiers.bitmap_query_threshold
+    kind = ctx.empty(m, torch.int8)
+    cap = ctx.empty(m, torch.int64)
+    alloc = ctx.empty(m, torch.int64)
+    ts = tiers_struct(tiers)
+    _lib.call("sg_plan", m, _PRED_CODE[pred_kind], ptr(pred), ptr(products), ptr(span_lo), ptr(span_hi),
+              ts, ptr(kind), ptr(cap), ptr(alloc), ctx.sp)
+    staging_bytes = int(alloc.sum().item()) * 12 if m else 0  # engine.py:259 rule
+    if cfg.staging_limit_bytes is not None and staging_bytes > cfg.staging_limit_bytes:
+        raise ResourceLimitError(
+            f"staged output needs {staging_bytes} bytes, over the {cfg.staging_limit_bytes} byte "
+            "limit; the symbolic workflow (workflow='symbolic') stages exact-sized rows")
+    counts = ctx.empty(m, torch.int64)
+    overflow = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
+    exact = pred_kind == "exact"
+    if exact:
+        row_ptr = scan(ctx, pred)
+        nnz_c = int(row_ptr[-1].item()) if m else 0
+        out_col = ctx.empty(nnz_c, torch.int32)
+        out_val = ctx.empty(nnz_c, dtype)
+        out_off = row_ptr
+    else:
+        main_alloc = torch.where(kind == int(PlanKind.FALLBACK), torch.zeros_like(alloc), alloc)
+        out_off = scan(ctx, main_alloc)
+        slab = int(out_off[-1].item()) if m else 0
+        out_col = ctx.empty(slab, torch.int32)
+        out_val = ctx.empty(slab, dtype)
+    if m:
+        _lib.call("sg_numeric", m, n, _dtype_code(A.values), ptr(A.row_ptr), ptr(A.col_idx), ptr(A.values),
+                  ptr(B.row_ptr), ptr(B.col_idx), ptr(B.values), ptr(kind), ptr(cap), ptr(alloc),
+                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(out_off), ptr(out_col), ptr(out_val),
+                  ptr(counts), ptr(overflow), ws, wsb, ctx.sp)
+    ev[4].record(ctx.stream)
+    ctx.sync()
+    t4 = time.perf_counter()
+    _check_deadline(deadline)
+
+    # ---- fallback (engine._fallback_phase): overflow | planned FALLBACK
+    fb_rows = ctx.empty(max(m, 1), torch.int64)
+    nfb = ctypes_int64()
+    if m:
+        _lib.call("sg_select_fallback", m, ptr(kind), ptr(products), ptr(overflow), ptr(fb_rows),
+                  nfb, ws, wsb, ctx.sp)
+    n_fb = int(nfb.value)
+    fb_rows = fb_rows[:n_fb]
+    fargs = (ptr(A.row_ptr), ptr(A.col_idx), ptr(A.values), ptr(B.row_ptr), ptr(B.col_idx), ptr(B.values),
+             ptr(products), ptr(span_lo), ptr(span_hi))
+    if exact:
+        if n_fb:
+            _lib.call("sg_fallback", 1, n_fb, ptr(fb_rows), n, _dtype_code(A.values), *fargs, ptr(row_ptr),
+                      ptr(out_col), ptr(out_val), ptr(counts), ws, wsb, ctx.sp)
+        C_col, C_val = out_col, out_val
+    else:
+        if n_fb:
+            _lib.call("sg_fallback", 0, n_fb, ptr(fb_rows), n, _dtype_code(A.values), *fargs, None, None, None,
+                      ptr(counts), ws, wsb, ctx.sp)
+        row_ptr = scan(ctx, counts)
+        nnz_c = int(row_ptr[-1].item()) if m else 0
+        C_col = ctx.empty(nnz_c, torch.int32)
+        C_val = ctx.empty(nnz_c, dtype)
+        if n_fb:
+            _lib.call("sg_fallback", 1, n_fb, ptr(fb_rows), n, _dtype_code(A.values), *fargs, ptr(row_ptr),
+                      ptr(C_col), ptr(C_val), ptr(counts), ws, wsb, ctx.sp)
+    ev[5].record(ctx.stream)
+    ctx.sync()
+    t5 = time.perf_counter()
+    _check_deadline(deadline)
+
+    # ---- post-processing: hash rows were sorted in-kernel; compact the slab
+    if not exact and m:
+        skip = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
+        if n_fb:
+            skip[fb_rows] = 1
+        _lib.call("sg_compact", m, _dtype_code(A.values), ptr(counts), ptr(skip), ptr(out_off), ptr(row_ptr),
+                  ptr(out_col), ptr(out_val), ptr(C_col), ptr(C_val), ctx.sp)
+        del out_col, out_val
+    if m == 0:
+        row_ptr = torch.zeros(1, dtype=torch.int64, device=ctx.device)
+        nnz_c = 0
+    ev[6].record(ctx.stream)
+    ctx.sync()
+    t6 = time.perf_counter()
+    for i, name in enumerate(("analysis", "sketch", "predict", "numeric", "fallback", "compact")):
+        kms[name] = ev[i].elapsed_time(ev[i + 1])
+
+    est_mean = est_std = None
+    if cfg.compute_estimation_errors and pred_kind == "estimated":
+        truth = (row_ptr[1:] - row_ptr[:-1]).to(torch.float64)
+        live = truth > 0
+        if bool(live.any()):
+            rel = (pred[live] - truth[live]).abs() / truth[live]
+            rel_h = rel.cpu().numpy()
+            est_mean, est_std = float(rel_h.mean()), float(rel_h.std())
+        else:
+            est_mean, est_std = 0.0, 0.0
+
+    Cd = DeviceCsr(m, n, row_ptr, C_col, C_val)
+    total_ms = (time.perf_counter() - t0) * 1e3
+    report = RunReport(
+        workflow=kind_wf.value, registers=registers, er=er,
+        cr_hat=None if cr is None else cr[0],
+        cr_true=(total_products / nnz_c) if nnz_c else None,
+        analysis_ms=(t1 - t0) * 1e3, sketch_ms=(t2 - t1) * 1e3 if regs is not None else 0.0,
+        predict_ms=(t3 - t2) * 1e3, numeric_ms=(t4 - t3) * 1e3, fallback_ms=(t5 - t4) * 1e3,
+        compact_ms=(t6 - t5) * 1e3, total_ms=total_ms, overflow_row_count=n_fb, nnz_c=nnz_c,
+        total_products=total_products, bitmap_query=bool(bitmap_query),
+        est_mean_rel_err=est_mean, est_std_rel_err=est_std,
+        gflops=(2.0 * total_products / (total_ms * 1e-3) / 1e9) if total_ms > 0 else None,
+        kernel_ms=kms)
+    if cfg.return_device:
+        return Cd, report
+    return Cd.to_host(), report
+
+
+def ctypes_int64():
+    import ctypes
+    return ctypes.c_int64(0)

@@ -1,0 +1,207 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference.
+
+Every golden case was produced by the real reference (tests/golden); structure
+must be bit-exact, values within rtol 1e-12 (fp64, atol 0; matgen.py:151-156),
+report fields equal.  Stage kernels are checked one by one against the
+reference's intermediates (row stats, sketches, estimates, exact counts,
+plans: all exact).
+"""
+import time
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from golden_io import Case, names  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+OVR = ("auto", "symbolic", "estimate", "upper")
+REPORT_EXACT = ("workflow", "registers", "overflow_row_count", "nnz_c", "total_products", "bitmap_query")
+REPORT_FLOAT = ("er", "cr_hat", "cr_true")
+
+
+def _cfg(o, tiers=None, **kw):
+    from paper_2604_19004_b200 import EngineConfig, WorkflowOverride
+    ov = {"auto": WorkflowOverride.AUTO, "symbolic": WorkflowOverride.FORCE_SYMBOLIC,
+          "estimate": WorkflowOverride.FORCE_ESTIMATE, "upper": WorkflowOverride.FORCE_UPPER_BOUND}[o]
+    if tiers is not None:
+        kw["tiers"] = tiers
+    return EngineConfig(workflow=ov, **kw)
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_19004_b200 import _lib
+    _lib.load()
+    return torch.device("cuda", 0)
+
+
+@pytest.mark.parametrize("name", names())
+def test_spgemm_matches_reference(gpu, name):
+    from paper_2604_19004_b200 import spgemm
+    c = Case(name)
+    for o in OVR:
+        C, rep = spgemm(c.A, c.B, _cfg(o, c.tiers()))
+        c.check_product(C)
+        want = c.meta["reports"][o]
+        for k in REPORT_EXACT:
+            assert getattr(rep, k) == want[k], (name, o, k, getattr(rep, k), want[k])
+        for k in REPORT_FLOAT:
+            got, exp = getattr(rep, k), want[k]
+            if exp is None:
+                assert got is None, (name, o, k)
+            else:
+                assert got == pytest.approx(exp, rel=1e-12), (name, o, k)
+
+
+@pytest.mark.parametrize("name", [n for n in names() if n.startswith(("pair", "corpus", "enh", "tiny", "bitmap"))])
+def test_stage_kernels_match_reference(gpu, name):
+    import paper_2604_19004_b200._lib as L
+    from paper_2604_19004_b200 import TierConfig
+    from paper_2604_19004_b200.device import ptr, to_device
+    from paper_2604_19004_b200.engine import _Ctx, hll_build, hll_estimate, row_stats, tiers_struct
+    c = Case(name)
+    ctx = _Ctx(gpu, torch.cuda.current_stream(gpu))
+    A = to_device(c.A, gpu)
+    B = to_device(c.B, gpu)
+    products, lo, hi, totals = row_stats(ctx, A, B)
+    np.testing.assert_array_equal(products.cpu().numpy(), c.d["products"])
+    np.testing.assert_array_equal(lo.cpu().numpy(), c.d["span_lo"])
+    np.testing.assert_array_equal(hi.cpu().numpy(), c.d["span_hi"])
+    assert int(totals[0]) == int(c.d["products"].sum())
+    for p in (5, 6, 7):
+        regs = hll_build(ctx, B, p)
+        np.testing.assert_array_equal(regs.cpu().numpy().reshape(B.nrows, 1 << p), c.d[f"regs_p{p}"])
+        est = hll_estimate(ctx, A, regs, p).cpu().numpy()
+        np.testing.assert_array_equal(est, c.d[f"est_p{p}"])  # bit-exact
+    m = A.nrows
+    ws, wsb = ctx.workspace(m)
+    exact = torch.empty(m, dtype=torch.int64, device=gpu)
+    L.call("sg_symbolic", m, B.ncols, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
+           ptr(products), ptr(lo), ptr(hi), ptr(exact), ws, wsb, ctx.sp)
+    np.testing.assert_array_equal(exact.cpu().numpy(), c.d["exact"])
+    t = c.tiers() or TierConfig()
+    est6 = hll_estimate(ctx, A, hll_build(ctx, B, 6), 6)
+    for wf, pred, code in (("symbolic", exact, 0), ("estimate", est6, 1), ("upper", products, 2)):
+        kind = torch.empty(m, dtype=torch.int8, device=gpu)
+        cap = torch.empty(m, dtype=torch.int64, device=gpu)
+        alloc = torch.empty(m, dtype=torch.int64, device=gpu)
+        L.call("sg_plan", m, code, ptr(pred), ptr(products), ptr(lo), ptr(hi), tiers_struct(t),
+               ptr(kind), ptr(cap), ptr(alloc), ctx.sp)
+        np.testing.assert_array_equal(kind.cpu().numpy(), c.d[f"plan_{wf}_kind"], err_msg=wf)
+        np.testing.assert_array_equal(cap.cpu().numpy(), c.d[f"plan_{wf}_cap"], err_msg=wf)
+        np.testing.assert_array_equal(alloc.cpu().numpy(), c.d[f"plan_{wf}_alloc"], err_msg=wf)
+
+
+def test_scan_kernel(gpu):
+    from paper_2604_19004_b200.engine import _Ctx, scan
+    ctx = _Ctx(gpu, torch.cuda.current_stream(gpu))
+    rng = np.random.default_rng(0)
+    for n in (0, 1, 5, 4095, 4096, 4097, 1_000_003):
+        x = rng.integers(0, 1 << 40, n)
+        out = scan(ctx, torch.from_numpy(x).to(gpu)).cpu().numpy()
+        np.testing.assert_array_equal(out, np.r_[0, np.cumsum(x)])
+
+
+def test_identity_and_errors(gpu):
+    from paper_2604_19004_b200 import (DeadlineExceeded, EngineConfig, ResourceLimitError, WorkflowOverride,
+                                       identity, spgemm, validate)
+    from oracle import ocean_cpu as oc
+    rng = np.random.default_rng(0)
+    rows = rng.integers(0, 25, 150)
+    cols = rng.integers(0, 40, 150)
+    b = oc.triplets_to_csr(25, 40, rows, cols, rng.uniform(0.5, 1.5, 150))
+    for o in OVR:
+        C, _ = spgemm(identity(25), b, _cfg(o))
+        np.testing.assert_array_equal(C.row_ptr, b.row_ptr)
+        np.testing.assert_array_equal(C.col_idx, b.col_idx)
+        np.testing.assert_array_equal(C.values, b.values)
+        assert validate(C) == []
+    with pytest.raises(ValueError, match="dimension"):
+        spgemm(identity(3), identity(4))
+    c = Case("pair00")
+    with pytest.raises(ResourceLimitError, match="symbolic"):
+        spgemm(c.A, c.B, EngineConfig(workflow=WorkflowOverride.FORCE_ESTIMATE, staging_limit_bytes=16))
+    with pytest.raises(DeadlineExceeded):
+        spgemm(c.A, c.B, EngineConfig(), deadline=time.perf_counter() - 1.0)
+
+
+def _random_pair(seed):
+    """Mixed generator in the spirit of pkg/tests/matgen.py:66-95 (restated)."""
+    from oracle import ocean_cpu as oc
+    rng = np.random.default_rng(seed)
+    kind = seed % 4
+    if kind == 0:
+        n, k, m = rng.integers(50, 3000, 3)
+        da, db = rng.uniform(0.001, 0.03, 2)
+    elif kind == 1:
+        n, k, m = 2000, 500, 40_000
+        da, db = 0.02, 0.004
+    elif kind == 2:
+        n, k, m = rng.integers(100, 1500, 3)
+        da, db = rng.uniform(0.01, 0.1, 2)
+    else:
+        n, k, m = 300, 20_000, 300_000
+        da, db = 0.002, 0.0005
+
+    def mk(r, c, d):
+        nnz = int(round(r * c * d))
+        lens = np.minimum((rng.pareto(1.4, r) + 0.2) * (nnz / r), c).astype(int)
+        rows = np.repeat(np.arange(r), lens)
+        cols = rng.integers(0, c, len(rows))
+        return oc.triplets_to_csr(r, c, rows, cols, rng.uniform(0.5, 1.5, len(rows)))
+    return mk(int(n), int(k), da), mk(int(k), int(m), db)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_skewed_pairs_vs_oracle(gpu, seed):
+    from paper_2604_19004_b200 import spgemm
+    from oracle import ocean_cpu as oc
+    a, b = _random_pair(seed)
+    ref, rrep = oc.spgemm(a, b)
+    for o in OVR:
+        C, rep = spgemm(a, b, _cfg(o))
+        np.testing.assert_array_equal(C.row_ptr, ref.row_ptr)
+        np.testing.assert_array_equal(C.col_idx, ref.col_idx)
+        np.testing.assert_allclose(C.values, ref.values, rtol=1e-12, atol=0)
+    _, rep = spgemm(a, b, _cfg("auto"))
+    assert rep.workflow == rrep["workflow"]
+    assert rep.overflow_row_count == rrep["overflow_row_count"]
+
+
+def test_tiny_tiers_overflow_rerun(gpu):
+    """Forced overflow with tiny tiers reruns through the fallback exactly
+    (pkg/tests/test_engine.py:280-292)."""
+    from paper_2604_19004_b200 import spgemm
+    c = Case("tiny_tiers")
+    C, rep = spgemm(c.A, c.B, _cfg("estimate", c.tiers()))
+    assert rep.overflow_row_count > 0
+    assert rep.overflow_row_count == c.meta["reports"]["estimate"]["overflow_row_count"]
+    c.check_product(C)
+
+
+def test_fp32_within_1e5(gpu):
+    from paper_2604_19004_b200 import EngineConfig, spgemm
+    c = Case("corpus0")
+    for o in OVR:
+        C, _ = spgemm(c.A, c.B, _cfg(o, dtype="f32"))
+        assert C.values.dtype == np.float32
+        c.check_product(C.astype(np.float64), rtol=1e-5)
+    del EngineConfig
+
+
+def test_config_scale_poisson_and_rmat_vs_oracle(gpu):
+    """Small instances of configs 2 and 3 through every workflow vs the oracle."""
+    from paper_2604_19004_b200 import matgen, spgemm
+    from oracle import ocean_cpu as oc
+    for a in (matgen.poisson27(16), matgen.rmat(12)):
+        ref, _ = oc.spgemm(a, a)
+        for o in OVR:
+            C, _ = spgemm(a, a, _cfg(o))
+            np.testing.assert_array_equal(C.row_ptr, ref.row_ptr)
+            np.testing.assert_array_equal(C.col_idx, ref.col_idx)
+            np.testing.assert_allclose(C.values, ref.values, rtol=1e-12, atol=0)
