@@ -28,6 +28,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# C of R-MAT-20 is 116 GB: avoid caching-allocator fragmentation between steps
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 
 def parse():
@@ -111,13 +113,17 @@ def rows_slice(a, lo, hi):
     return CsrMatrix(hi - lo, a.ncols, a.row_ptr[lo:hi + 1] - s, a.col_idx[s:e], a.values[s:e])
 
 
+def row_products(a, b):
+    """Intermediate products per row of A (host, for sharding and sampling)."""
+    cum = np.r_[0, np.cumsum(np.diff(b.row_ptr)[a.col_idx])]
+    return cum[a.row_ptr[1:]] - cum[a.row_ptr[:-1]]
+
+
 def cpu_sample_blocks(a, b, target_products):
     """Deterministic products-stratified row blocks: one block from the head
     (hub rows of an unpermuted R-MAT), one from the middle and one from the
     tail of the products prefix, each about target/3 products."""
-    bn = np.diff(b.row_ptr)
-    per = np.add.reduceat(bn[a.col_idx], a.row_ptr[:-1]) if a.nnz else np.zeros(a.nrows, np.int64)
-    per = np.where(np.diff(a.row_ptr) > 0, per, 0)
+    per = row_products(a, b)
     cum = np.r_[0, np.cumsum(per)]
     total = int(cum[-1])
     if total <= target_products:
@@ -210,9 +216,7 @@ def main():
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     vbytes = 8 if args.dtype == "f64" else 4
     # shard rows by balanced products (north star: row-sharded, B replicated)
-    bn = np.diff(b.row_ptr)
-    per = np.add.reduceat(bn[a.col_idx], a.row_ptr[:-1]) if a.nnz else np.zeros(a.nrows, np.int64)
-    per = np.where(np.diff(a.row_ptr) > 0, per, 0)
+    per = row_products(a, b)
     cum = np.r_[0, np.cumsum(per)]
     total_products = int(cum[-1])
     cuts = [int(np.searchsorted(cum, total_products * r / n_gpus, side="left")) for r in range(n_gpus + 1)]
@@ -280,29 +284,33 @@ def main():
 
     # e2e through the public API with host buffers (H2D + D2H inside the timed region)
     e2e = None
+    torch.cuda.empty_cache()
     if not args.no_e2e:
-        cfg_h = EngineConfig(dtype=args.dtype)
-        a_h = a_loc if args.dtype == "f64" else a_loc.astype(np.float32)
-        b_h = (a_h if (same and n_gpus == 1) else (b if args.dtype == "f64" else b.astype(np.float32)))
-        ts = []
-        cbytes = 0
-        for _ in range(max(1, args.e2e_steps)):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            ch, rh = spgemm(a_h, b_h, cfg_h)
-            torch.cuda.synchronize()
-            ts.append(time.perf_counter() - t0)
-            cbytes = ch.row_ptr.nbytes + ch.col_idx.nbytes + ch.values.nbytes
-            del ch
-        h2d = a_h.row_ptr.nbytes + a_h.col_idx.nbytes + a_h.values.nbytes
-        if b_h is not a_h:
-            h2d += b_h.row_ptr.nbytes + b_h.col_idx.nbytes + b_h.values.nbytes
-        tw = torch.tensor([max(ts) if world > 1 else float(np.mean(ts))], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
-        e2e = {"value": 2.0 * products / float(tw[0]) / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(cbytes),
-               "seconds_per_step": float(tw[0])}
+        try:
+            cfg_h = EngineConfig(dtype=args.dtype)
+            a_h = a_loc if args.dtype == "f64" else a_loc.astype(np.float32)
+            b_h = (a_h if (same and n_gpus == 1) else (b if args.dtype == "f64" else b.astype(np.float32)))
+            ts = []
+            cbytes = 0
+            for _ in range(max(1, args.e2e_steps)):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                ch, rh = spgemm(a_h, b_h, cfg_h)
+                torch.cuda.synchronize()
+                ts.append(time.perf_counter() - t0)
+                cbytes = ch.row_ptr.nbytes + ch.col_idx.nbytes + ch.values.nbytes
+                del ch
+            h2d = a_h.row_ptr.nbytes + a_h.col_idx.nbytes + a_h.values.nbytes
+            if b_h is not a_h:
+                h2d += b_h.row_ptr.nbytes + b_h.col_idx.nbytes + b_h.values.nbytes
+            tw = torch.tensor([max(ts) if world > 1 else float(np.mean(ts))], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+            e2e = {"value": 2.0 * products / float(tw[0]) / 1e9, "unit": "GFLOP/s",
+                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(cbytes),
+                   "seconds_per_step": float(tw[0])}
+        except Exception as exc:  # reported in the JSON line, never dropped silently
+            e2e = {"value": None, "unit": "GFLOP/s", "error": f"{type(exc).__name__}: {exc}"[:300]}
 
     cpu = None
     if rank == 0 and n_gpus == 1 and not args.no_cpu:

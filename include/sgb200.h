@@ -91,12 +91,36 @@ int sg_hll_estimate(int64_t nsel, const int64_t* rows, const int64_t* a_ptr,
                     const int32_t* a_col, const uint8_t* regs, int p, const double* lin_table,
                     double alpha_mm, double* est, void* stream);
 
+/* Numeric windows for long rows.  sg_window_capacity sizes, per row, the
+ * window list the count kernels may emit (rows with select[row] != 0, or all
+ * rows when select == NULL): win_off int64[m+1] (exclusive scan of the
+ * capacities), *total_host = win_off[m].  The caller allocates wins as
+ * int32[2 * total] filled with -1 and nwin int32[m] filled with 0. */
+int sg_window_capacity(int64_t m, const int64_t* products, const int64_t* span_lo,
+                       const int64_t* span_hi, const uint8_t* select, int64_t* win_off,
+                       int64_t* total_host, void* ws, size_t ws_bytes, void* stream);
+
 /* Replaces predict.symbolic_pass (predict.py:39-84): exact distinct output
- * columns per row of C (counts int64[m]). */
+ * columns per row of C (counts int64[m]).  When win_off/wins/nwin are given,
+ * rows counted with a bitmap also record their numeric windows (pairs of
+ * (first column, rank of that column in the row); each window holds at most
+ * 6144 distinct columns over at most 262144 columns). */
 int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col,
                 const int64_t* b_ptr, const int32_t* b_col, const int64_t* products,
-                const int64_t* span_lo, const int64_t* span_hi, int64_t* counts, void* ws,
-                size_t ws_bytes, void* stream);
+                const int64_t* span_lo, const int64_t* span_hi, int64_t* counts,
+                const int64_t* win_off, int32_t* wins, int32_t* nwin, void* ws, size_t ws_bytes,
+                void* stream);
+
+/* Long-row numeric pass over the windows recorded by sg_symbolic /
+ * sg_fallback(mode 0): one CTA per (row, window), values accumulated in
+ * shared memory, written sorted at out_off[row] + rank (out_off = row_ptr of
+ * C).  work_buf: int32[2 * work_cap] scratch, work_cap >= total windows. */
+int sg_window_numeric(int64_t m, int dtype, const int64_t* a_ptr, const int32_t* a_col,
+                      const void* a_val, const int64_t* b_ptr, const int32_t* b_col,
+                      const void* b_val, const int64_t* span_hi, const int64_t* win_off,
+                      const int32_t* wins, const int32_t* nwin, const int64_t* out_off,
+                      int32_t* out_col, void* out_val, int32_t* work_buf, int64_t work_cap,
+                      void* ws, size_t ws_bytes, void* stream);
 
 /* Replaces accumulate.plan_rows (accumulate.py:104-181) with the identical
  * integer rules.  pred is int64 (EXACT / UPPER) or f64 (ESTIMATED). */
@@ -114,30 +138,35 @@ int sg_scan(int64_t n, const int64_t* in, int64_t* out, void* ws, size_t ws_byte
  * are sorted in-kernel: engine._sort_hash_rows, engine.py:331-343).
  * counts[row] = distinct count (0 if overflowed); overflow[row] = 1 when the
  * reference's tier limit is exceeded (hash: count > floor(0.8*cap); dense:
- * count > alloc). */
+ * count > alloc).  Rows with skip_nwin[row] > 0 (nullable) are left to
+ * sg_window_numeric. */
 int sg_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, const int32_t* a_col,
                const void* a_val, const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
                const int8_t* kind, const int64_t* cap, const int64_t* alloc,
                const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
                const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts,
-               uint8_t* overflow, void* ws, size_t ws_bytes, void* stream);
+               uint8_t* overflow, const int32_t* skip_nwin, void* ws, size_t ws_bytes,
+               void* stream);
 
 /* Rows for the fallback pass (engine.py:202-203): overflow | (kind ==
- * FALLBACK & products > 0), ascending; *n_out_host receives the count. */
+ * FALLBACK & products > 0), ascending, minus rows with exclude_nwin[row] > 0
+ * (nullable); *n_out_host receives the count. */
 int sg_select_fallback(int64_t m, const int8_t* kind, const int64_t* products,
-                       const uint8_t* overflow, int64_t* rows_out, int64_t* n_out_host, void* ws,
-                       size_t ws_bytes, void* stream);
+                       const uint8_t* overflow, const int32_t* exclude_nwin, int64_t* rows_out,
+                       int64_t* n_out_host, void* ws, size_t ws_bytes, void* stream);
 
 /* Replaces engine._fallback_phase (engine.py:312-328) /
  * accumulate.fallback_accumulate (accumulate.py:274-279): exact accumulation
  * of the given rows, which can never overflow.  mode 0 = count only
- * (counts[row] written), mode 1 = numeric, written sorted at out_off[row]. */
+ * (counts[row] written; numeric windows recorded when win_off/wins/nwin are
+ * given, as in sg_symbolic), mode 1 = numeric, written sorted at out_off[row]. */
 int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, int dtype,
                 const int64_t* a_ptr, const int32_t* a_col, const void* a_val,
                 const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
                 const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
                 const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts,
-                void* ws, size_t ws_bytes, void* stream);
+                const int64_t* win_off, int32_t* wins, int32_t* nwin, void* ws, size_t ws_bytes,
+                void* stream);
 
 /* Replaces engine.compact (engine.py:346-368): copy counts[row] entries of
  * every row with skip[row] == 0 from src_off[row] to dst_off[row]. */

@@ -36,12 +36,14 @@ SIGNATURES = {
     "sg_row_stats": (I32, [I64, I64, P, P, P, P, P, P, P, P, P]),
     "sg_hll_build": (I32, [I64, P, P, I32, P, P]),
     "sg_hll_estimate": (I32, [I64, P, P, P, P, I32, P, D, P, P]),
-    "sg_symbolic": (I32, [I64, I64, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "sg_window_capacity": (I32, [I64, P, P, P, P, P, C.POINTER(C.c_int64), P, SZ, P]),
+    "sg_symbolic": (I32, [I64, I64, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "sg_window_numeric": (I32, [I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P, SZ, P]),
     "sg_plan": (I32, [I64, I32, P, P, P, P, C.POINTER(SgTiers), P, P, P, P]),
     "sg_scan": (I32, [I64, P, P, P, SZ, P]),
-    "sg_numeric": (I32, [I64, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
-    "sg_select_fallback": (I32, [I64, P, P, P, P, C.POINTER(C.c_int64), P, SZ, P]),
-    "sg_fallback": (I32, [I32, I64, P, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "sg_numeric": (I32, [I64, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "sg_select_fallback": (I32, [I64, P, P, P, P, P, C.POINTER(C.c_int64), P, SZ, P]),
+    "sg_fallback": (I32, [I32, I64, P, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "sg_compact": (I32, [I64, I32, P, P, P, P, P, P, P, P, P]),
 }
 

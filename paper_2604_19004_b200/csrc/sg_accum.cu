@@ -76,24 +76,40 @@ __device__ __forceinline__ void warp_products(const Entries& E, int nent, int64_
   }
   int c0 = lo;
   const unsigned le = lanemask_le();
-  for (int64_t p0 = pbeg; p0 < pend; p0 += 32) {
-    const int ci = c0 + 1 + lane;
-    const int64_t nxt = ci < nent ? E.S[ci] : (int64_t)NOLIMIT;
-    const int64_t d = nxt - p0;
-    const unsigned bit = d < 32 ? (1u << (unsigned)d) : 0u;
-    const unsigned mask = __reduce_or_sync(SG_FULL, bit);
-    const int c = c0 + __popc(mask & le);
-    const int64_t p = p0 + lane;
-    if (p < pend) {
-      const int64_t j = E.bs[c] + (p - E.S[c]);
-      const int32_t col = __ldg(b_col + j);
-      double v = 0.0;
-      if (VALUES) v = E.av[c] * (double)__ldg(b_val + j);
-      op(col, v);
+  // UNR steps of 32 products per iteration: owners are resolved first (shared
+  // memory + CREDUX only), then all UNR global loads are issued back to back
+  // so several L2/HBM round trips are in flight per lane.
+  constexpr int UNR = 4;
+  for (int64_t p0 = pbeg; p0 < pend; p0 += 32 * UNR) {
+    int64_t jj[UNR];
+    int cc[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int64_t q0 = p0 + 32 * u;
+      const int ci = c0 + 1 + lane;
+      const int64_t nxt = ci < nent ? E.S[ci] : (int64_t)NOLIMIT;
+      const int64_t d = nxt - q0;
+      const unsigned bit = (d >= 0 && d < 32) ? (1u << (unsigned)d) : 0u;
+      const unsigned mask = __reduce_or_sync(SG_FULL, bit);
+      const int c = c0 + __popc(mask & le);
+      const int64_t p = q0 + lane;
+      cc[u] = c;
+      jj[u] = (p < pend) ? E.bs[c] + (p - E.S[c]) : -1;
+      const int k = __popc(mask);
+      const int64_t nk = __shfl_sync(SG_FULL, nxt, k);
+      c0 = c0 + k + (nk == q0 + 32 ? 1 : 0);
+      if (c0 >= nent) c0 = nent - 1;
     }
-    const int k = __popc(mask);
-    const int64_t nk = __shfl_sync(SG_FULL, nxt, k);
-    c0 = c0 + k + (nk == p0 + 32 ? 1 : 0);
+    int32_t col[UNR];
+    double bv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      col[u] = jj[u] >= 0 ? __ldg(b_col + jj[u]) : 0;
+      bv[u] = (VALUES && jj[u] >= 0) ? (double)__ldg(b_val + jj[u]) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+      if (jj[u] >= 0) op(col[u], VALUES ? E.av[cc[u]] * bv[u] : 0.0);
   }
 }
 
@@ -548,6 +564,48 @@ struct BitmapAddOp {
   }
 };
 
+// Exclusive prefix of word popcounts: pre[i] = set bits in words [0, i);
+// returns the total.  Warps own contiguous word ranges and read them with
+// consecutive lanes (no bank conflicts).
+template <int NT>
+__device__ __forceinline__ int64_t bitmap_prefix(const unsigned long long* bm, int* pre, int nwords,
+                                                 int64_t* scr) {
+  constexpr int NW = NT / 32;
+  const int w = warp_id(), lane = lane_id();
+  const int per = ((nwords + NW - 1) / NW + 31) & ~31;
+  const int wb = min(nwords, per * w), we = min(nwords, per * (w + 1));
+  int64_t s = 0;
+  for (int i = wb + lane; i < we; i += 32) s += __popcll(bm[i]);
+  s = warp_sum(s);
+  int64_t tot;
+  int64_t base = block_excl_scan(lane == 0 ? s : (int64_t)0, scr, &tot);
+  base = __shfl_sync(SG_FULL, base, 0);
+  for (int i0 = wb; i0 < we; i0 += 32) {
+    const int i = i0 + lane;
+    const int v = i < we ? __popcll(bm[i]) : 0;
+    const int inc = warp_incl_scan(v);
+    if (i < we) pre[i] = (int)(base + inc - v);
+    base += __shfl_sync(SG_FULL, inc, 31);
+  }
+  __syncthreads();
+  return tot;
+}
+
+// Numeric window geometry (shared by the count kernels that emit windows and
+// the window accumulator): a window holds at most WIN_R distinct columns and
+// spans at most WIN_WORDS*64 columns, so its bitmap, rank prefix and values
+// all sit in shared memory.
+constexpr int WIN_WORDS = 4096;  // 262,144 columns
+constexpr int WIN_R = 6144;      // values per window (48 KB fp64)
+constexpr int WIN_RP = WIN_R - 64;
+constexpr int WIN_NT = 512;
+
+__host__ __device__ __forceinline__ int64_t window_capacity(int64_t products, int64_t span) {
+  if (products <= 0 || span <= 0) return 0;
+  const int64_t d = products < span ? products : span;
+  return d / WIN_RP + ((span - 1) / 64) / WIN_WORDS + 1;
+}
+
 template <int BW, int MODE, typename V, int NT>
 __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __restrict__ rows, Csr A, Csr B,
                                                const int8_t* kind, const int64_t* cap, const int64_t* alloc,
@@ -555,7 +613,9 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
                                                const int64_t* __restrict__ span_hi,
                                                const int64_t* __restrict__ out_off,
                                                int32_t* __restrict__ out_col, V* __restrict__ out_val,
-                                               int64_t* __restrict__ counts, uint8_t* __restrict__ overflow) {
+                                               int64_t* __restrict__ counts, uint8_t* __restrict__ overflow,
+                                               const int64_t* __restrict__ win_off, int2* __restrict__ wins,
+                                               int32_t* __restrict__ nwin) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int64_t scr[NT / 32 + 2];
   unsigned long long* bm = reinterpret_cast<unsigned long long*>(smem);
@@ -564,12 +624,14 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
   Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (NT + 1),
             reinterpret_cast<double*>(ebase) + 2 * (NT + 1)};
   constexpr int64_t WCOLS = (int64_t)BW * 64;
-  constexpr int WPT = (BW + NT - 1) / NT;  // words per thread
+  __shared__ int64_t last_id;
   for (int64_t b = blockIdx.x; b < nbin; b += gridDim.x) {
     const int64_t row = rows[b];
     const int64_t lo = span_lo[row], hi = span_hi[row];
     const int64_t limit = row_limit(kind, cap, alloc, row);
     int64_t total = 0;
+    const int64_t wcap = (MODE == 0 && win_off) ? win_off[row + 1] - win_off[row] : 0;
+    if (threadIdx.x == 0) last_id = -1;
     const bool multi = hi - lo + 1 > WCOLS;
     // count-only sweep first when a limit applies and the span needs windows
     bool over = false;
@@ -606,28 +668,43 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
       __syncthreads();
       BitmapSetOp<V> so{bm, wlo, whi};
       block_row<false, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, so, nullptr);
-      // per-thread contiguous words -> exclusive prefix of popcounts
-      int64_t c = 0;
-      const int w0 = threadIdx.x * WPT;
-#pragma unroll 4
-      for (int i = 0; i < WPT; ++i)
-        if (w0 + i < nwords) c += __popcll(bm[w0 + i]);
-      int64_t wtot;
-      int64_t run = block_excl_scan(c, scr, &wtot);
-      if (MODE == 0) {
+      if (MODE == 0 && wcap == 0) {
+        int64_t c = 0;
+        for (int i = threadIdx.x; i < nwords; i += NT) c += __popcll(bm[i]);
+        int64_t wtot;
+        block_excl_scan(c, scr, &wtot);
         total += wtot;
+        continue;
+      }
+      const int64_t wtot = bitmap_prefix<NT>(bm, pre, nwords, scr);
+      if (MODE == 0) {
+        // emit numeric windows: word gw (relative to lo) starts window
+        // id = rank/WIN_RP + gw/WIN_WORDS whenever the id changes
+        const int64_t gw0 = (wlo - lo) >> 6;
+        int2* wrow = wins + win_off[row];
+        const int64_t prev_last = last_id;
+        __syncthreads();
+        for (int i = threadIdx.x; i < nwords; i += NT) {
+          const int64_t gw = gw0 + i;
+          const int64_t rank = total + pre[i];
+          const int64_t id = rank / WIN_RP + gw / WIN_WORDS;
+          int64_t idp = -1;
+          if (i > 0) {
+            idp = (total + pre[i - 1]) / WIN_RP + (gw - 1) / WIN_WORDS;
+          } else if (gw > 0) {
+            idp = prev_last;
+          }
+          if (id != idp && id < wcap) wrow[id] = make_int2((int)(lo + 64 * gw), (int)rank);
+          if (i == nwords - 1) last_id = id;
+        }
+        total += wtot;
+        __syncthreads();
         continue;
       }
       if (!multi && total + wtot > limit) {
         over = true;
         break;
       }
-      for (int i = 0; i < WPT; ++i)
-        if (w0 + i < nwords) {
-          pre[w0 + i] = (int)run;
-          run += __popcll(bm[w0 + i]);
-        }
-      __syncthreads();
       const int64_t base = out_off[row] + total;
       // emit sorted columns from the bitmap and clear the value slots
       for (int i = threadIdx.x; i < nwords; i += NT) {
@@ -648,6 +725,7 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
     if (threadIdx.x == 0) {
       if (MODE == 0) {
         counts[row] = total;
+        if (wcap > 0) nwin[row] = (int32_t)(last_id + 1);
       } else {
         counts[row] = over ? 0 : total;
         if (overflow) overflow[row] = over ? 1 : 0;
@@ -660,6 +738,214 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
 template <int BW, int NT>
 constexpr size_t bm_smem() {
   return (size_t)BW * 12 + (size_t)3 * (NT + 1) * 8;
+}
+
+// -------------------------------------------------------------------------
+// BMW: rank-window accumulator for long rows (multi-block per row).
+//
+// The count pass (k_bitmap, MODE 0) leaves, per long row, a list of windows
+// (first column, rank of that column within the row) such that every window
+// holds <= WIN_R distinct columns over <= WIN_WORDS*64 columns.  One CTA per
+// (row, window) work item: restrict every selected B row to the window's
+// column range (binary search), build the window bitmap (ATOMS.OR), rank
+// prefix, accumulate values in shared memory at rank (fp64), then write the
+// window's sorted slice of C with coalesced stores.  Windows of one row run
+// on different SMs, so a 9.7M-product hub row is spread over ~80 CTAs.
+
+__device__ __forceinline__ int64_t lower_bound_col(const int32_t* __restrict__ col, int64_t s, int64_t e,
+                                                   int64_t c) {
+  while (s < e) {
+    const int64_t mid = (s + e) >> 1;
+    if ((int64_t)__ldg(col + mid) < c) s = mid + 1; else e = mid;
+  }
+  return s;
+}
+
+// Load a chunk of A entries whose B rows are clipped to columns [c0, c1).
+template <bool VALUES, typename V>
+__device__ __forceinline__ int64_t block_load_range(int64_t t, int64_t t1, int64_t c0, int64_t c1,
+                                                    const int32_t* __restrict__ a_col,
+                                                    const V* __restrict__ a_val,
+                                                    const int64_t* __restrict__ b_ptr,
+                                                    const int32_t* __restrict__ b_col, Entries E,
+                                                    int64_t* scr, int& nent) {
+  int64_t bs = 0, len = 0;
+  double av = 0.0;
+  if (t + threadIdx.x < t1) {
+    const int32_t k = a_col[t + threadIdx.x];
+    const int64_t s = b_ptr[k], e = b_ptr[k + 1];
+    if (e > s) {
+      const int64_t f = __ldg(b_col + s), l = __ldg(b_col + e - 1);
+      if (l >= c0 && f < c1) {
+        const int64_t ss = f >= c0 ? s : lower_bound_col(b_col, s, e, c0);
+        const int64_t ee = l < c1 ? e : lower_bound_col(b_col, ss, e, c1);
+        bs = ss;
+        len = ee - ss;
+      }
+    }
+    if (VALUES) av = (double)a_val[t + threadIdx.x];
+  }
+  int64_t P, n64;
+  const int64_t S = block_excl_scan(len, scr, &P);
+  const int64_t pos = block_excl_scan((int64_t)(len > 0), scr, &n64);
+  if (len > 0) {
+    E.S[pos] = S;
+    E.bs[pos] = bs;
+    if (VALUES) E.av[pos] = av;
+  }
+  __syncthreads();
+  nent = (int)n64;
+  return P;
+}
+
+template <bool VALUES, typename V, class Op>
+__device__ __forceinline__ void block_chunk_products(const Entries& E, int nent, int64_t P,
+                                                     const int32_t* __restrict__ b_col,
+                                                     const V* __restrict__ b_val, Op& op) {
+  const int nw = blockDim.x >> 5, w = warp_id();
+  const int64_t per = ((P + nw - 1) / nw + 31) & ~(int64_t)31;
+  warp_products<VALUES, V>(E, nent, min(P, per * w), min(P, per * (w + 1)), b_col, b_val, op);
+}
+
+struct WinSetOp {
+  unsigned* bm32;
+  int64_t c0;
+  __device__ __forceinline__ void operator()(int32_t col, double) {
+    const int64_t x = col - c0;
+    atomicOr(bm32 + (x >> 5), 1u << (x & 31));
+  }
+};
+
+struct WinAddOp {
+  const unsigned long long* bm;
+  const int* pre;
+  double* vals;
+  int64_t c0;
+  __device__ __forceinline__ void operator()(int32_t col, double v) {
+    const int64_t x = col - c0;
+    const int w = (int)(x >> 6);
+    const int r = pre[w] + __popcll(bm[w] & ((1ull << (x & 63)) - 1ull));
+    smem_add(&vals[r], v);
+  }
+};
+
+constexpr size_t bmw_smem() {
+  return (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8 + (size_t)3 * (WIN_NT + 1) * 8;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(WIN_NT, 2) k_bmw(int64_t nwork, const int2* __restrict__ work, Csr A, Csr B,
+                                                   const int64_t* __restrict__ span_hi,
+                                                   const int64_t* __restrict__ win_off,
+                                                   const int2* __restrict__ wins, const int32_t* __restrict__ nwin,
+                                                   const int64_t* __restrict__ out_off,
+                                                   int32_t* __restrict__ out_col, V* __restrict__ out_val,
+                                                   unsigned long long* __restrict__ ticket) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int64_t scr[WIN_NT / 32 + 2];
+  __shared__ int64_t item;
+  unsigned long long* bm = reinterpret_cast<unsigned long long*>(smem);
+  int* pre = reinterpret_cast<int*>(smem + (size_t)WIN_WORDS * 8);
+  double* vals = reinterpret_cast<double*>(smem + (size_t)WIN_WORDS * 12);
+  unsigned char* ebase = smem + (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8;
+  Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (WIN_NT + 1),
+            reinterpret_cast<double*>(ebase) + 2 * (WIN_NT + 1)};
+  const V* av = (const V*)A.val;
+  const V* bv = (const V*)B.val;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) item = (int64_t)atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const int64_t b = item;
+    if (b >= nwork) return;
+    const int64_t row = work[b].x;
+    const int id = work[b].y;
+    const int2* wr = wins + win_off[row];
+    const int n = nwin[row];
+    const int2 me = wr[id];
+    if (me.x < 0) continue;
+    int64_t c1 = span_hi[row] + 1;
+    int64_t rend = out_off[row + 1] - out_off[row];
+    for (int j = id + 1; j < n; ++j) {
+      const int2 nx = wr[j];
+      if (nx.x >= 0) {
+        c1 = nx.x;
+        rend = nx.y;
+        break;
+      }
+    }
+    const int64_t c0 = me.x;
+    const int cnt = (int)(rend - me.y);
+    const int nwords = (int)((c1 - c0 + 63) >> 6);
+    for (int i = threadIdx.x; i < nwords; i += WIN_NT) bm[i] = 0ull;
+    for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
+    __syncthreads();
+    const int64_t t0 = A.ptr[row], t1 = A.ptr[row + 1];
+    const bool single = (t1 - t0) <= WIN_NT;
+    WinSetOp so{reinterpret_cast<unsigned*>(bm), c0};
+    int nent = 0;
+    int64_t P = 0;
+    if (single) {
+      P = block_load_range<true, V>(t0, t1, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
+      block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
+      __syncthreads();
+    } else {
+      for (int64_t t = t0; t < t1; t += WIN_NT) {
+        P = block_load_range<false, V>(t, t1, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
+        block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
+        __syncthreads();
+      }
+    }
+    bitmap_prefix<WIN_NT>(bm, pre, nwords, scr);
+    WinAddOp ao{bm, pre, vals, c0};
+    if (single) {
+      block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
+      __syncthreads();
+    } else {
+      for (int64_t t = t0; t < t1; t += WIN_NT) {
+        P = block_load_range<true, V>(t, t1, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
+        block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
+        __syncthreads();
+      }
+    }
+    const int64_t base = out_off[row] + me.y;
+    for (int i = threadIdx.x; i < nwords; i += WIN_NT) {
+      unsigned long long bits = bm[i];
+      int64_t pos = base + pre[i];
+      while (bits) {
+        const int bb = __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        out_col[pos++] = (int32_t)(c0 + (int64_t)i * 64 + bb);
+      }
+    }
+    for (int i = threadIdx.x; i < cnt; i += WIN_NT) out_val[base + i] = (V)vals[i];
+    __syncthreads();
+  }
+}
+
+// work list: (row, window id) for every row with windows
+__global__ void k_win_counts(int64_t m, const int32_t* __restrict__ nwin, int64_t* __restrict__ n_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) n_out[i] = nwin[i] > 0 ? nwin[i] : 0;
+}
+
+__global__ void k_win_scatter(int64_t m, const int32_t* __restrict__ nwin, const int64_t* __restrict__ off,
+                              int2* __restrict__ work) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int n = nwin[i];
+  const int64_t o = off[i];
+  for (int j = 0; j < n; ++j) work[o + j] = make_int2((int)i, j);
+}
+
+__global__ void k_win_capacity(int64_t m, const int64_t* __restrict__ products, const int64_t* __restrict__ lo,
+                               const int64_t* __restrict__ hi, const uint8_t* __restrict__ select,
+                               int64_t* __restrict__ cap) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int64_t p = products[i];
+  const bool sel = (select == nullptr || select[i]) && p > 256;
+  cap[i] = sel ? window_capacity(p, hi[i] - lo[i] + 1) : 0;
 }
 
 // -------------------------------------------------------------------------
@@ -721,13 +1007,14 @@ __global__ void k_classify_numeric(int64_t m, const int8_t* __restrict__ kind, c
                                    const int64_t* __restrict__ alloc, const int64_t* __restrict__ products,
                                    const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
                                    uint8_t* __restrict__ bins, int64_t* __restrict__ counts,
-                                   uint8_t* __restrict__ overflow) {
+                                   uint8_t* __restrict__ overflow, const int32_t* __restrict__ nwin) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int64_t p = products[i];
   const int8_t k = kind[i];
   uint8_t b;
-  if (p == 0 || k == SG_KIND_FALLBACK) {
+  // rows with numeric windows (exact counts known) go to the window kernel
+  if (p == 0 || k == SG_KIND_FALLBACK || (nwin && nwin[i] > 0)) {
     b = BIN_NONE;
     counts[i] = 0;
     overflow[i] = 0;
@@ -801,6 +1088,9 @@ struct Launch {
   int64_t* counts;
   uint8_t* overflow;
   cudaStream_t s;
+  const int64_t* win_off = nullptr;  // count mode: emit numeric windows
+  int2* wins = nullptr;
+  int32_t* nwin = nullptr;
 };
 
 template <int LOG2T, int MODE, typename V>
@@ -831,7 +1121,8 @@ static int launch_bm(const Launch& L, const int32_t* rows, int64_t n) {
   if (int rc = set_smem(kern, sm)) return rc;
   int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 32);
   kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.lo, L.hi, L.out_off, L.out_col,
-                           (V*)L.out_val, L.counts, L.overflow);
+                           (V*)L.out_val, L.counts, L.overflow, MODE == 0 ? L.win_off : nullptr,
+                           MODE == 0 ? L.wins : nullptr, MODE == 0 ? L.nwin : nullptr);
   return check_cuda("k_bitmap");
 }
 
@@ -901,7 +1192,8 @@ extern "C" {
 
 int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col, const int64_t* b_ptr,
                 const int32_t* b_col, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
-                int64_t* counts, void* ws, size_t ws_bytes, void* stream) {
+                int64_t* counts, const int64_t* win_off, int32_t* wins, int32_t* nwin, void* ws,
+                size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   if (m == 0) return SG_OK;
@@ -910,6 +1202,9 @@ int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t*
   if (int rc = check_cuda("k_classify_count")) return rc;
   Launch L{{a_ptr, a_col, nullptr}, {b_ptr, b_col, nullptr}, nullptr, nullptr, nullptr, span_lo, span_hi,
            nullptr, nullptr, nullptr, counts, nullptr, s};
+  L.win_off = win_off;
+  L.wins = reinterpret_cast<int2*>(wins);
+  L.nwin = nwin;
   (void)b_ncols;
   return run_bins<0, double>(L, m, w, nullptr);
 }
@@ -918,14 +1213,15 @@ int sg_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, cons
                const void* a_val, const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
                const int8_t* kind, const int64_t* cap, const int64_t* alloc, const int64_t* products,
                const int64_t* span_lo, const int64_t* span_hi, const int64_t* out_off, int32_t* out_col,
-               void* out_val, int64_t* counts, uint8_t* overflow, void* ws, size_t ws_bytes, void* stream) {
+               void* out_val, int64_t* counts, uint8_t* overflow, const int32_t* skip_nwin, void* ws,
+               size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   if (m == 0) return SG_OK;
   (void)b_ncols;
   cudaStream_t s = (cudaStream_t)stream;
   k_classify_numeric<<<grid_for(m, 256), 256, 0, s>>>(m, kind, cap, alloc, products, span_lo, span_hi, w.bins,
-                                                      counts, overflow);
+                                                      counts, overflow, skip_nwin);
   if (int rc = check_cuda("k_classify_numeric")) return rc;
   Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, kind, cap, alloc, span_lo, span_hi,
            out_off, out_col, out_val, counts, overflow, s};
@@ -938,8 +1234,8 @@ int sg_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, cons
 int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, int dtype, const int64_t* a_ptr,
                 const int32_t* a_col, const void* a_val, const int64_t* b_ptr, const int32_t* b_col,
                 const void* b_val, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
-                const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts, void* ws,
-                size_t ws_bytes, void* stream) {
+                const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts,
+                const int64_t* win_off, int32_t* wins, int32_t* nwin, void* ws, size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, nrows, w)) return SG_ERR_WORKSPACE;
   if (nrows == 0) return SG_OK;
@@ -956,6 +1252,11 @@ int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, i
   if (int rc = check_cuda("k_gather_rows")) return rc;
   Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, nullptr, nullptr, nullptr, span_lo, span_hi,
            out_off, out_col, out_val, counts, nullptr, s};
+  if (mode == 0) {
+    L.win_off = win_off;
+    L.wins = reinterpret_cast<int2*>(wins);
+    L.nwin = nwin;
+  }
   for (int b : kOrder) {
     if (cnt[b] == 0) continue;
     int rc;
@@ -968,6 +1269,65 @@ int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, i
     if (rc) return rc;
   }
   return SG_OK;
+}
+
+int sg_window_capacity(int64_t m, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
+                       const uint8_t* select, int64_t* win_off, int64_t* total_host, void* ws, size_t ws_bytes,
+                       void* stream) {
+  Workspace w;
+  if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (m > 0) {
+    k_win_capacity<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, select, w.tmp);
+    if (int rc = check_cuda("k_win_capacity")) return rc;
+  }
+  if (int rc = scan_i64(m, w.tmp, win_off, w.partials, s)) return rc;
+  cudaMemcpyAsync(total_host, win_off + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_capacity sync", 0);
+  return SG_OK;
+}
+
+int sg_window_numeric(int64_t m, int dtype, const int64_t* a_ptr, const int32_t* a_col, const void* a_val,
+                      const int64_t* b_ptr, const int32_t* b_col, const void* b_val, const int64_t* span_hi,
+                      const int64_t* win_off, const int32_t* wins, const int32_t* nwin, const int64_t* out_off,
+                      int32_t* out_col, void* out_val, int32_t* work_buf, int64_t work_cap, void* ws,
+                      size_t ws_bytes, void* stream) {
+  Workspace w;
+  if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
+  if (m == 0) return SG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_win_counts<<<grid_for(m, 256), 256, 0, s>>>(m, nwin, w.tmp);
+  if (int rc = check_cuda("k_win_counts")) return rc;
+  if (int rc = scan_i64(m, w.tmp, w.tmp, w.partials, s)) return rc;
+  int64_t nwork = 0;
+  cudaMemcpyAsync(&nwork, w.tmp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric sync", 0);
+  if (nwork == 0) return SG_OK;
+  if (nwork > work_cap) {
+    set_error("sg_window_numeric: work buffer too small");
+    return SG_ERR_WORKSPACE;
+  }
+  int2* work = reinterpret_cast<int2*>(work_buf);
+  k_win_scatter<<<grid_for(m, 256), 256, 0, s>>>(m, nwin, w.tmp, work);
+  if (int rc = check_cuda("k_win_scatter")) return rc;
+  unsigned long long* ticket = reinterpret_cast<unsigned long long*>(w.bincnt);
+  cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s);
+  constexpr size_t sm = bmw_smem();
+  const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
+  const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms() * 2);
+  const int2* wn = reinterpret_cast<const int2*>(wins);
+  if (dtype == SG_F64) {
+    auto kern = k_bmw<double>;
+    if (int rc = set_smem(kern, sm)) return rc;
+    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, span_hi, win_off, wn, nwin, out_off, out_col,
+                                  (double*)out_val, ticket);
+  } else {
+    auto kern = k_bmw<float>;
+    if (int rc = set_smem(kern, sm)) return rc;
+    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, span_hi, win_off, wn, nwin, out_off, out_col,
+                                  (float*)out_val, ticket);
+  }
+  return check_cuda("k_bmw");
 }
 
 }  // extern "C"

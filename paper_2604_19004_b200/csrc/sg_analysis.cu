@@ -378,19 +378,26 @@ int partition_rows(int64_t m, int nbins, Workspace& w, int64_t* cnt_host, int64_
 // ---------------------------------------------------------------------------
 // fallback-row selection and compaction
 
+__device__ __forceinline__ bool is_fallback_row(int64_t i, const int8_t* kind, const int64_t* products,
+                                                const uint8_t* overflow, const int32_t* exclude) {
+  const bool fb = (overflow && overflow[i]) || (kind[i] == SG_KIND_FALLBACK && products[i] > 0);
+  return fb && !(exclude && exclude[i] > 0);
+}
+
 __global__ void k_fb_flags(int64_t m, const int8_t* __restrict__ kind, const int64_t* __restrict__ products,
-                           const uint8_t* __restrict__ overflow, int64_t* __restrict__ flags) {
+                           const uint8_t* __restrict__ overflow, const int32_t* __restrict__ exclude,
+                           int64_t* __restrict__ flags) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
-  flags[i] = ((overflow && overflow[i]) || (kind[i] == SG_KIND_FALLBACK && products[i] > 0)) ? 1 : 0;
+  flags[i] = is_fallback_row(i, kind, products, overflow, exclude) ? 1 : 0;
 }
 
 __global__ void k_fb_scatter(int64_t m, const int8_t* __restrict__ kind, const int64_t* __restrict__ products,
-                             const uint8_t* __restrict__ overflow, const int64_t* __restrict__ pos,
-                             int64_t* __restrict__ rows_out) {
+                             const uint8_t* __restrict__ overflow, const int32_t* __restrict__ exclude,
+                             const int64_t* __restrict__ pos, int64_t* __restrict__ rows_out) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
-  if ((overflow && overflow[i]) || (kind[i] == SG_KIND_FALLBACK && products[i] > 0)) rows_out[pos[i]] = i;
+  if (is_fallback_row(i, kind, products, overflow, exclude)) rows_out[pos[i]] = i;
 }
 
 template <typename V>
@@ -492,7 +499,8 @@ int sg_scan(int64_t n, const int64_t* in, int64_t* out, void* ws, size_t ws_byte
 }
 
 int sg_select_fallback(int64_t m, const int8_t* kind, const int64_t* products, const uint8_t* overflow,
-                       int64_t* rows_out, int64_t* n_out_host, void* ws, size_t ws_bytes, void* stream) {
+                       const int32_t* exclude_nwin, int64_t* rows_out, int64_t* n_out_host, void* ws,
+                       size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
@@ -501,13 +509,11 @@ int sg_select_fallback(int64_t m, const int8_t* kind, const int64_t* products, c
     return SG_OK;
   }
   int g = grid_for(m, 256);
-  k_fb_flags<<<g, 256, 0, s>>>(m, kind, products, overflow, w.tmp);
-  // scan in place into a second region: reuse partials for tiles; output
-  // positions go to rowlist-sized int64 space -> use tmp as input, write the
-  // scan back into tmp (k_scan_down reads `in` before writing `out` per tile)
+  k_fb_flags<<<g, 256, 0, s>>>(m, kind, products, overflow, exclude_nwin, w.tmp);
+  // in-place scan of the flags (k_scan_down reads its tile before writing it)
   int rc = scan_i64(m, w.tmp, w.tmp, w.partials, s);
   if (rc) return rc;
-  k_fb_scatter<<<g, 256, 0, s>>>(m, kind, products, overflow, w.tmp, rows_out);
+  k_fb_scatter<<<g, 256, 0, s>>>(m, kind, products, overflow, exclude_nwin, w.tmp, rows_out);
   count_launches(2);
   cudaMemcpyAsync(n_out_host, w.tmp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_select_fallback sync");

@@ -141,6 +141,40 @@ def scan(ctx: _Ctx, x):
     return out
 
 
+class Windows:
+    """Numeric window table of the long rows (see include/sgb200.h)."""
+
+    def __init__(self, off, wins, nwin, total):
+        self.off, self.wins, self.nwin, self.total = off, wins, nwin, total
+
+    def args(self):
+        return ptr(self.off), ptr(self.wins), ptr(self.nwin)
+
+
+def windows(ctx: _Ctx, m, products, lo, hi, select) -> Windows:
+    off = ctx.empty(m + 1, torch.int64)
+    total = ctypes_int64()
+    ws, wsb = ctx.workspace(max(m, 1))
+    _lib.call("sg_window_capacity", m, ptr(products), ptr(lo), ptr(hi), ptr(select), ptr(off), total,
+              ws, wsb, ctx.sp)
+    total = int(total.value)
+    wins = torch.full((max(2 * total, 2),), -1, dtype=torch.int32, device=ctx.device)
+    nwin = torch.zeros(max(m, 1), dtype=torch.int32, device=ctx.device)
+    return Windows(off, wins, nwin, total)
+
+
+def select_fallback(ctx: _Ctx, m, kind, products, overflow, exclude):
+    """Fallback rows (engine.py:202-203), optionally minus rows with windows."""
+    rows = ctx.empty(max(m, 1), torch.int64)
+    n = ctypes_int64()
+    if m:
+        ws, wsb = ctx.workspace(m)
+        _lib.call("sg_select_fallback", m, ptr(kind), ptr(products), ptr(overflow), ptr(exclude), ptr(rows),
+                  n, ws, wsb, ctx.sp)
+    n = int(n.value)
+    return rows[:n], n
+
+
 def _dtype_code(v: torch.Tensor) -> int:
     return 0 if v.dtype == torch.float64 else 1
 
@@ -169,12 +203,12 @@ def spgemm(a, b, cfg: EngineConfig | None = None, deadline: float | None = None)
 
 
 def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
-    dtype = torch.float64
-    if cfg.dtype == "f32" or (cfg.dtype is None and np.dtype(getattr(a.values, "dtype", np.float64)) == np.float32
-                              and not isinstance(a, DeviceCsr)):
-        dtype = torch.float32
-    if isinstance(a, DeviceCsr) and cfg.dtype is None:
+    if cfg.dtype is not None:
+        dtype = torch.float64 if cfg.dtype == "f64" else torch.float32
+    elif isinstance(a, DeviceCsr):
         dtype = a.values.dtype
+    else:
+        dtype = torch.float32 if np.asarray(a.values).dtype == np.float32 else torch.float64
     kms = {}
     t0 = time.perf_counter()
     A = to_device(a, ctx.device, dtype)
@@ -231,10 +265,12 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
 
     # ---- size prediction (predict.py)
     ws, wsb = ctx.workspace(max(m, 1))
+    win = None
     if kind_wf is WorkflowKind.SYMBOLIC:
         pred = ctx.empty(m, torch.int64)
+        win = windows(ctx, m, products, span_lo, span_hi, None)
         _lib.call("sg_symbolic", m, n, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
-                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(pred), ws, wsb, ctx.sp)
+                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(pred), *win.args(), ws, wsb, ctx.sp)
         pred_kind = "exact"
     elif kind_wf is WorkflowKind.HLL_ESTIMATION:
         pred = hll_estimate(ctx, A, regs, p)
@@ -267,6 +303,8 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     counts = ctx.empty(m, torch.int64)
     overflow = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
     exact = pred_kind == "exact"
+    dcode = _dtype_code(A.values)
+    Aargs = (ptr(A.row_ptr), ptr(A.col_idx), ptr(A.values), ptr(B.row_ptr), ptr(B.col_idx), ptr(B.values))
     if exact:
         row_ptr = scan(ctx, pred)
         nnz_c = int(row_ptr[-1].item()) if m else 0
@@ -280,41 +318,40 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         out_col = ctx.empty(slab, torch.int32)
         out_val = ctx.empty(slab, dtype)
     if m:
-        _lib.call("sg_numeric", m, n, _dtype_code(A.values), ptr(A.row_ptr), ptr(A.col_idx), ptr(A.values),
-                  ptr(B.row_ptr), ptr(B.col_idx), ptr(B.values), ptr(kind), ptr(cap), ptr(alloc),
+        _lib.call("sg_numeric", m, n, dcode, *Aargs, ptr(kind), ptr(cap), ptr(alloc),
                   ptr(products), ptr(span_lo), ptr(span_hi), ptr(out_off), ptr(out_col), ptr(out_val),
-                  ptr(counts), ptr(overflow), ws, wsb, ctx.sp)
+                  ptr(counts), ptr(overflow), ptr(win.nwin) if win else None, ws, wsb, ctx.sp)
     ev[4].record(ctx.stream)
     ctx.sync()
     t4 = time.perf_counter()
     _check_deadline(deadline)
 
-    # ---- fallback (engine._fallback_phase): overflow | planned FALLBACK
-    fb_rows = ctx.empty(max(m, 1), torch.int64)
-    nfb = ctypes_int64()
-    if m:
-        _lib.call("sg_select_fallback", m, ptr(kind), ptr(products), ptr(overflow), ptr(fb_rows),
-                  nfb, ws, wsb, ctx.sp)
-    n_fb = int(nfb.value)
-    fb_rows = fb_rows[:n_fb]
-    fargs = (ptr(A.row_ptr), ptr(A.col_idx), ptr(A.values), ptr(B.row_ptr), ptr(B.col_idx), ptr(B.values),
-             ptr(products), ptr(span_lo), ptr(span_hi))
+    # ---- fallback (engine._fallback_phase): overflow | planned FALLBACK rows
+    fb_rows, n_fb = select_fallback(ctx, m, kind, products, overflow, None)
+    fargs = (*Aargs, ptr(products), ptr(span_lo), ptr(span_hi))
     if exact:
-        if n_fb:
-            _lib.call("sg_fallback", 1, n_fb, ptr(fb_rows), n, _dtype_code(A.values), *fargs, ptr(row_ptr),
-                      ptr(out_col), ptr(out_val), ptr(counts), ws, wsb, ctx.sp)
         C_col, C_val = out_col, out_val
     else:
+        # count the fallback rows (recording windows for long ones), size C
+        sel = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
         if n_fb:
-            _lib.call("sg_fallback", 0, n_fb, ptr(fb_rows), n, _dtype_code(A.values), *fargs, None, None, None,
-                      ptr(counts), ws, wsb, ctx.sp)
+            sel[fb_rows] = 1
+        win = windows(ctx, m, products, span_lo, span_hi, sel)
+        if n_fb:
+            _lib.call("sg_fallback", 0, n_fb, ptr(fb_rows), n, dcode, *fargs, None, None, None,
+                      ptr(counts), *win.args(), ws, wsb, ctx.sp)
         row_ptr = scan(ctx, counts)
         nnz_c = int(row_ptr[-1].item()) if m else 0
         C_col = ctx.empty(nnz_c, torch.int32)
         C_val = ctx.empty(nnz_c, dtype)
-        if n_fb:
-            _lib.call("sg_fallback", 1, n_fb, ptr(fb_rows), n, _dtype_code(A.values), *fargs, ptr(row_ptr),
-                      ptr(C_col), ptr(C_val), ptr(counts), ws, wsb, ctx.sp)
+    if win is not None and win.total:
+        work = ctx.empty(2 * win.total, torch.int32)
+        _lib.call("sg_window_numeric", m, dcode, *Aargs, ptr(span_hi), *win.args(), ptr(row_ptr),
+                  ptr(C_col), ptr(C_val), ptr(work), win.total, ws, wsb, ctx.sp)
+    rest, n_rest = (fb_rows, n_fb) if win is None else select_fallback(ctx, m, kind, products, overflow, win.nwin)
+    if n_rest:
+        _lib.call("sg_fallback", 1, n_rest, ptr(rest), n, dcode, *fargs, ptr(row_ptr),
+                  ptr(C_col), ptr(C_val), ptr(counts), None, None, None, ws, wsb, ctx.sp)
     ev[5].record(ctx.stream)
     ctx.sync()
     t5 = time.perf_counter()

@@ -1,0 +1,201 @@
+"""Row-sharded multi-GPU SpGEMM: one process per GPU.
+
+Gustavson rows are independent (chunk independence is asserted
+at engine.py:13-14), so C = A*B shards by rows of A with no exchange in the
+data path:
+
+  1. the root rank holds A and B; B (and A when it differs) is broadcast to
+     every rank — ncclBroadcast over NVLink/NVSwitch via torch.distributed;
+  2. rows of A are cut into contiguous ranges with balanced intermediate-
+     product counts (the products prefix from the row-stats kernel on root);
+  3. every rank runs the single-GPU pipeline (engine.spgemm) on its rows;
+  4. offset exchange: all_gather of one int64 nnz per rank -> each shard's
+     global row_ptr offset (the "stitch");
+  5. optionally the shards are gathered to the root (NCCL send/recv) when C
+     fits there; otherwise C stays distributed (R-MAT-23's C is ~2 TB).
+
+The per-rank multiply is pluggable (``local_fn``) so the host logic — the
+partition, broadcast, offset exchange and stitching — is tested on CPU with
+gloo at world size 2 (tests/test_shard_gloo.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class Shard:
+    """One rank's rows of C plus the stitching metadata."""
+
+    row_lo: int
+    row_hi: int
+    nnz_offset: int          # global index of this shard's first entry
+    nnz_total: int           # nnz of the whole C
+    row_ptr: torch.Tensor    # local row_ptr (starts at 0)
+    col_idx: torch.Tensor
+    values: torch.Tensor
+    report: object = None
+
+
+def balanced_cuts(products: np.ndarray, parts: int) -> list:
+    """Contiguous row ranges with near-equal product sums (row r of rank i is
+    in [cuts[i], cuts[i+1]))."""
+    n = len(products)
+    cum = np.concatenate(([0], np.cumsum(products, dtype=np.int64)))
+    total = int(cum[-1])
+    cuts = [0]
+    for r in range(1, parts):
+        cuts.append(int(np.searchsorted(cum, total * r / parts, side="left")))
+    cuts.append(n)
+    for i in range(1, len(cuts)):  # monotone
+        cuts[i] = max(cuts[i], cuts[i - 1])
+    return cuts
+
+
+def _bcast_tensor(t, shape, dtype, device, src, group):
+    if t is None:
+        t = torch.empty(shape, dtype=dtype, device=device)
+    dist.broadcast(t, src=src, group=group)
+    return t
+
+
+def broadcast_csr(m, device, src, group):
+    """Broadcast a CSR (host or device arrays on `src`) to every rank as
+    device tensors.  Returns (nrows, ncols, row_ptr, col_idx, values)."""
+    rank = dist.get_rank(group)
+    if rank == src:
+        meta = torch.tensor([m.nrows, m.ncols, int(m.row_ptr[-1]),
+                             0 if np.dtype(_np_dtype(m.values)) == np.float64 else 1],
+                            dtype=torch.int64, device=device)
+    else:
+        meta = torch.empty(4, dtype=torch.int64, device=device)
+    dist.broadcast(meta, src=src, group=group)
+    nrows, ncols, nnz, dt = (int(x) for x in meta.tolist())
+    vdt = torch.float64 if dt == 0 else torch.float32
+    if rank == src:
+        rp = _as_tensor(m.row_ptr, torch.int64, device)
+        ci = _as_tensor(m.col_idx, torch.int32, device)
+        vv = _as_tensor(m.values, vdt, device)
+    else:
+        rp = ci = vv = None
+    rp = _bcast_tensor(rp, (nrows + 1,), torch.int64, device, src, group)
+    ci = _bcast_tensor(ci, (nnz,), torch.int32, device, src, group)
+    vv = _bcast_tensor(vv, (nnz,), vdt, device, src, group)
+    return nrows, ncols, rp, ci, vv
+
+
+def _np_dtype(v):
+    return v.dtype if isinstance(v, np.ndarray) else {torch.float64: np.float64,
+                                                      torch.float32: np.float32}[v.dtype]
+
+
+def _as_tensor(x, dtype, device):
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(x)).to(device=device, dtype=dtype)
+
+
+def row_products(a_ptr: torch.Tensor, a_col: torch.Tensor, b_ptr: torch.Tensor) -> np.ndarray:
+    """Products per row of A (analysis.py:100-104) for partitioning, as a
+    gather + cumsum over torch tensors (used on CPU test ranks; the GPU path
+    uses the row-stats kernel)."""
+    bn = (b_ptr[1:] - b_ptr[:-1])
+    per_nz = bn[a_col.long()]
+    cum = torch.cat([torch.zeros(1, dtype=torch.int64, device=per_nz.device), torch.cumsum(per_nz, 0)])
+    return (cum[a_ptr[1:]] - cum[a_ptr[:-1]]).cpu().numpy()
+
+
+def spgemm_sharded(a, b, local_fn, group=None, root=0, device=None, gather=False, products_fn=None):
+    """Row-sharded C = A*B over the ranks of `group`.
+
+    ``a`` / ``b`` are needed on ``root`` only (host CsrMatrix or DeviceCsr; the
+    other ranks pass None).  ``local_fn(nrows, ncols, row_ptr, col_idx,
+    values, B) -> (row_ptr, col_idx, values, report)`` multiplies this rank's
+    rows.  Returns the local ``Shard``; with ``gather=True`` the root's return
+    value is the full C as a Shard covering all rows.
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    device = device or torch.device("cpu")
+    same = rank == root and (b is a)
+    flag = torch.tensor([1 if same else 0], dtype=torch.int64, device=device)
+    dist.broadcast(flag, src=root, group=group)
+    same = bool(flag.item())
+    B = broadcast_csr(b if rank == root else None, device, root, group)
+    A = B if same else broadcast_csr(a if rank == root else None, device, root, group)
+    # balanced cuts computed on the root and broadcast
+    cuts_t = torch.empty(world + 1, dtype=torch.int64, device=device)
+    if rank == root:
+        per = (products_fn or row_products)(A[2], A[3], B[2])
+        cuts_t.copy_(torch.tensor(balanced_cuts(per, world), dtype=torch.int64))
+    dist.broadcast(cuts_t, src=root, group=group)
+    cuts = [int(x) for x in cuts_t.tolist()]
+    lo, hi = cuts[rank], cuts[rank + 1]
+    s, e = int(A[2][lo].item()), int(A[2][hi].item())
+    a_rp = (A[2][lo:hi + 1] - s).contiguous()
+    rp, ci, vv, rep = local_fn(hi - lo, A[1], a_rp, A[3][s:e].contiguous(), A[4][s:e].contiguous(), B)
+    # offset exchange: one int64 per rank
+    nnz = torch.tensor([int(ci.numel())], dtype=torch.int64, device=device)
+    all_nnz = [torch.zeros_like(nnz) for _ in range(world)]
+    dist.all_gather(all_nnz, nnz, group=group)
+    counts = [int(x.item()) for x in all_nnz]
+    offset = int(sum(counts[:rank]))
+    shard = Shard(lo, hi, offset, int(sum(counts)), rp, ci, vv, rep)
+    if not gather:
+        return shard
+    return gather_shards(shard, counts, cuts, root, group, device)
+
+
+def gather_shards(shard: Shard, counts, cuts, root, group, device):
+    """Stitch the shards into one CSR on `root` (NCCL/gloo point-to-point)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if rank != root:
+        if shard.col_idx.numel():
+            dist.send(shard.col_idx, dst=root, group=group)
+            dist.send(shard.values, dst=root, group=group)
+        dist.send(shard.row_ptr, dst=root, group=group)
+        return shard
+    nrows = cuts[-1]
+    total = int(sum(counts))
+    col = torch.empty(total, dtype=shard.col_idx.dtype, device=device)
+    val = torch.empty(total, dtype=shard.values.dtype, device=device)
+    row_ptr = torch.empty(nrows + 1, dtype=torch.int64, device=device)
+    off = 0
+    for r in range(world):
+        lo, hi = cuts[r], cuts[r + 1]
+        n = counts[r]
+        if r == rank:
+            col[off:off + n] = shard.col_idx
+            val[off:off + n] = shard.values
+            rp = shard.row_ptr
+        else:
+            if n:
+                dist.recv(col[off:off + n], src=r, group=group)
+                dist.recv(val[off:off + n], src=r, group=group)
+            rp = torch.empty(hi - lo + 1, dtype=torch.int64, device=device)
+            dist.recv(rp, src=r, group=group)
+        row_ptr[lo:hi + 1] = rp + off
+        off += n
+    return Shard(0, nrows, 0, total, row_ptr, col, val, shard.report)
+
+
+def gpu_local_fn(cfg):
+    """local_fn running the single-GPU engine on this rank's device."""
+    from .device import DeviceCsr
+    from .engine import spgemm
+    from dataclasses import replace
+
+    cfg = replace(cfg, return_device=True)
+
+    def fn(nrows, ncols_a, row_ptr, col_idx, values, B):
+        Ad = DeviceCsr(nrows, ncols_a, row_ptr, col_idx, values)
+        Bd = DeviceCsr(B[0], B[1], B[2], B[3], B[4])
+        c, rep = spgemm(Ad, Bd, cfg)
+        return c.row_ptr, c.col_idx, c.values, rep
+    return fn
