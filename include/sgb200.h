@@ -91,36 +91,52 @@ int sg_hll_estimate(int64_t nsel, const int64_t* rows, const int64_t* a_ptr,
                     const int32_t* a_col, const uint8_t* regs, int p, const double* lin_table,
                     double alpha_mm, double* est, void* stream);
 
-/* Numeric windows for long rows.  sg_window_capacity sizes, per row, the
- * window list the count kernels may emit (rows with select[row] != 0, or all
- * rows when select == NULL): win_off int64[m+1] (exclusive scan of the
- * capacities), *total_host = win_off[m].  The caller allocates wins as
- * int32[2 * total] filled with -1 and nwin int32[m] filled with 0. */
+/* Numeric windows of long rows, recorded by the count kernels (sg_symbolic,
+ * sg_fallback mode 0) and consumed by sg_window_numeric.
+ *  win_off  int64[m+1]  window-slot offsets (from sg_window_capacity)
+ *  wins     int32[2*win_off[m]] (first column, rank in row) pairs, init -1
+ *  nwin     int32[m]    slots used per row, init 0
+ *  bm_off   int64[m+1]  word offsets of saved key bitmaps, or NULL
+ *  bm_save  uint64[bm_off[m]] saved key bitmaps, or NULL (then the numeric
+ *           pass rebuilds each window's key bitmap from the products)
+ * Each window holds at most 16384 distinct columns over at most 262144
+ * columns, so its bitmap, rank prefix and values sit in shared memory. */
+typedef struct sg_windows {
+  const int64_t* win_off;
+  int32_t* wins;
+  int32_t* nwin;
+  const int64_t* bm_off;
+  uint64_t* bm_save;
+} sg_windows_t;
+
+/* Sizes the window tables for rows with select[row] != 0 (all rows when
+ * select == NULL): writes win_off and, if bm_off != NULL, bm_off (both
+ * int64[m+1] exclusive scans); totals_host[0] = win_off[m],
+ * totals_host[1] = bm_off[m] (0 without bm_off). */
 int sg_window_capacity(int64_t m, const int64_t* products, const int64_t* span_lo,
                        const int64_t* span_hi, const uint8_t* select, int64_t* win_off,
-                       int64_t* total_host, void* ws, size_t ws_bytes, void* stream);
+                       int64_t* bm_off, int64_t* totals_host, void* ws, size_t ws_bytes,
+                       void* stream);
 
 /* Replaces predict.symbolic_pass (predict.py:39-84): exact distinct output
- * columns per row of C (counts int64[m]).  When win_off/wins/nwin are given,
- * rows counted with a bitmap also record their numeric windows (pairs of
- * (first column, rank of that column in the row); each window holds at most
- * 6144 distinct columns over at most 262144 columns). */
+ * columns per row of C (counts int64[m]).  With win != NULL, rows counted
+ * with a bitmap also record their numeric windows (and save their bitmaps
+ * when win->bm_save != NULL). */
 int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col,
                 const int64_t* b_ptr, const int32_t* b_col, const int64_t* products,
                 const int64_t* span_lo, const int64_t* span_hi, int64_t* counts,
-                const int64_t* win_off, int32_t* wins, int32_t* nwin, void* ws, size_t ws_bytes,
-                void* stream);
+                const sg_windows_t* win, void* ws, size_t ws_bytes, void* stream);
 
-/* Long-row numeric pass over the windows recorded by sg_symbolic /
- * sg_fallback(mode 0): one CTA per (row, window), values accumulated in
- * shared memory, written sorted at out_off[row] + rank (out_off = row_ptr of
- * C).  work_buf: int32[2 * work_cap] scratch, work_cap >= total windows. */
+/* Long-row numeric pass over the recorded windows: one CTA per run of <= 8
+ * windows of a row, values accumulated in shared memory (fp64), columns and
+ * values written sorted at out_off[row] + rank (out_off = row_ptr of C).
+ * work_buf: 120 bytes x work_cap scratch, work_cap >= total windows. */
 int sg_window_numeric(int64_t m, int dtype, const int64_t* a_ptr, const int32_t* a_col,
                       const void* a_val, const int64_t* b_ptr, const int32_t* b_col,
-                      const void* b_val, const int64_t* span_hi, const int64_t* win_off,
-                      const int32_t* wins, const int32_t* nwin, const int64_t* out_off,
-                      int32_t* out_col, void* out_val, int32_t* work_buf, int64_t work_cap,
-                      void* ws, size_t ws_bytes, void* stream);
+                      const void* b_val, const int64_t* span_lo, const int64_t* span_hi,
+                      const sg_windows_t* win, const int64_t* out_off, int32_t* out_col,
+                      void* out_val, void* work_buf, int64_t work_cap, void* ws, size_t ws_bytes,
+                      void* stream);
 
 /* Replaces accumulate.plan_rows (accumulate.py:104-181) with the identical
  * integer rules.  pred is int64 (EXACT / UPPER) or f64 (ESTIMATED). */
@@ -158,15 +174,14 @@ int sg_select_fallback(int64_t m, const int8_t* kind, const int64_t* products,
 /* Replaces engine._fallback_phase (engine.py:312-328) /
  * accumulate.fallback_accumulate (accumulate.py:274-279): exact accumulation
  * of the given rows, which can never overflow.  mode 0 = count only
- * (counts[row] written; numeric windows recorded when win_off/wins/nwin are
- * given, as in sg_symbolic), mode 1 = numeric, written sorted at out_off[row]. */
+ * (counts[row] written; numeric windows recorded when win != NULL, as in
+ * sg_symbolic), mode 1 = numeric, written sorted at out_off[row]. */
 int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, int dtype,
                 const int64_t* a_ptr, const int32_t* a_col, const void* a_val,
                 const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
                 const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
                 const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts,
-                const int64_t* win_off, int32_t* wins, int32_t* nwin, void* ws, size_t ws_bytes,
-                void* stream);
+                const sg_windows_t* win, void* ws, size_t ws_bytes, void* stream);
 
 /* Replaces engine.compact (engine.py:346-368): copy counts[row] entries of
  * every row with skip[row] == 0 from src_off[row] to dst_off[row]. */

@@ -13,12 +13,17 @@ import threading
 
 from .config import CudaLibraryError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsgb200.so")
+LIB_PATH = os.environ.get("SGB200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsgb200.so")
 
 _lock = threading.Lock()
 _lib = None
 
 I64, I32, SZ, P, D = C.c_int64, C.c_int, C.c_size_t, C.c_void_p, C.c_double
+
+
+class SgWindows(C.Structure):
+    _fields_ = [("win_off", C.c_void_p), ("wins", C.c_void_p), ("nwin", C.c_void_p),
+                ("bm_off", C.c_void_p), ("bm_save", C.c_void_p)]
 
 
 class SgTiers(C.Structure):
@@ -36,14 +41,16 @@ SIGNATURES = {
     "sg_row_stats": (I32, [I64, I64, P, P, P, P, P, P, P, P, P]),
     "sg_hll_build": (I32, [I64, P, P, I32, P, P]),
     "sg_hll_estimate": (I32, [I64, P, P, P, P, I32, P, D, P, P]),
-    "sg_window_capacity": (I32, [I64, P, P, P, P, P, C.POINTER(C.c_int64), P, SZ, P]),
-    "sg_symbolic": (I32, [I64, I64, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
-    "sg_window_numeric": (I32, [I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P, SZ, P]),
+    "sg_window_capacity": (I32, [I64, P, P, P, P, P, P, P, P, SZ, P]),
+    "sg_symbolic": (I32, [I64, I64, P, P, P, P, P, P, P, P, C.POINTER(SgWindows), P, SZ, P]),
+    "sg_window_numeric": (I32, [I64, I32, P, P, P, P, P, P, P, P, C.POINTER(SgWindows), P, P, P, P, I64,
+                                P, SZ, P]),
     "sg_plan": (I32, [I64, I32, P, P, P, P, C.POINTER(SgTiers), P, P, P, P]),
     "sg_scan": (I32, [I64, P, P, P, SZ, P]),
     "sg_numeric": (I32, [I64, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "sg_select_fallback": (I32, [I64, P, P, P, P, P, C.POINTER(C.c_int64), P, SZ, P]),
-    "sg_fallback": (I32, [I32, I64, P, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "sg_fallback": (I32, [I32, I64, P, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P,
+                          C.POINTER(SgWindows), P, SZ, P]),
     "sg_compact": (I32, [I64, I32, P, P, P, P, P, P, P, P, P]),
 }
 

@@ -81,6 +81,30 @@ __device__ __forceinline__ void warp_products(const Entries& E, int nent, int64_
   // so several L2/HBM round trips are in flight per lane.
   constexpr int UNR = 4;
   for (int64_t p0 = pbeg; p0 < pend; p0 += 32 * UNR) {
+    // fast path (warp-uniform): the whole 32*UNR block lies in one B-row
+    // segment, so lane products are consecutive elements of that row and no
+    // owner search is needed.  Long B rows (hubs) take this path.
+    const int64_t blk_end = min(p0 + 32 * UNR, pend);
+    const int64_t seg_end = (c0 + 1 < nent) ? E.S[c0 + 1] : (int64_t)NOLIMIT;
+    if (seg_end >= blk_end) {
+      const int64_t base = E.bs[c0] + (p0 - E.S[c0]) + lane;
+      const double a = VALUES ? E.av[c0] : 0.0;
+      const int64_t nvalid = blk_end - p0;
+      int32_t col[UNR];
+      double bv[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const bool ok = 32 * u + lane < nvalid;
+        col[u] = ok ? __ldg(b_col + base + 32 * u) : 0;
+        bv[u] = (VALUES && ok) ? (double)__ldg(b_val + base + 32 * u) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u)
+        if (32 * u + lane < nvalid) op(col[u], VALUES ? a * bv[u] : 0.0);
+      if (seg_end == blk_end) ++c0;
+      if (c0 >= nent) c0 = nent - 1;
+      continue;
+    }
     int64_t jj[UNR];
     int cc[UNR];
 #pragma unroll
@@ -591,14 +615,46 @@ __device__ __forceinline__ int64_t bitmap_prefix(const unsigned long long* bm, i
   return tot;
 }
 
+// Write the column of every set bit of a 64-bit bitmap word, ascending.
+__device__ __forceinline__ void emit_bits(unsigned long long bits, int32_t colbase, int32_t* __restrict__ out) {
+  unsigned lo = (unsigned)bits, hi = (unsigned)(bits >> 32);
+  int k = 0;
+  while (lo) {
+    out[k++] = colbase + __ffs(lo) - 1;
+    lo &= lo - 1;
+  }
+  while (hi) {
+    out[k++] = colbase + 31 + __ffs(hi);
+    hi &= hi - 1;
+  }
+}
+
 // Numeric window geometry (shared by the count kernels that emit windows and
 // the window accumulator): a window holds at most WIN_R distinct columns and
 // spans at most WIN_WORDS*64 columns, so its bitmap, rank prefix and values
 // all sit in shared memory.
 constexpr int WIN_WORDS = 4096;  // 262,144 columns
-constexpr int WIN_R = 6144;      // values per window (48 KB fp64)
+constexpr int WIN_R = 16384;     // values per window (128 KB fp64)
 constexpr int WIN_RP = WIN_R - 64;
-constexpr int WIN_NT = 512;
+constexpr int WIN_NT = 1024;
+
+// device view of sg_windows_t (include/sgb200.h)
+struct Win {
+  const int64_t* off;
+  int2* wins;
+  int32_t* nwin;
+  const int64_t* bm_off;
+  unsigned long long* bm_save;
+};
+
+// Symbolic-pass routing: rows counted with a shared-memory bitmap (and hence
+// able to record numeric windows).  Long rows with a dense enough span, and
+// every row too long for the largest count hash table.
+__host__ __device__ __forceinline__ bool count_uses_bitmap(int64_t p, int64_t span) {
+  if (p <= 1024) return false;
+  if (span <= ((int64_t)1 << 20) && (span + 63) / 64 <= p) return true;
+  return p > 16384;
+}
 
 __host__ __device__ __forceinline__ int64_t window_capacity(int64_t products, int64_t span) {
   if (products <= 0 || span <= 0) return 0;
@@ -614,8 +670,10 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
                                                const int64_t* __restrict__ out_off,
                                                int32_t* __restrict__ out_col, V* __restrict__ out_val,
                                                int64_t* __restrict__ counts, uint8_t* __restrict__ overflow,
-                                               const int64_t* __restrict__ win_off, int2* __restrict__ wins,
-                                               int32_t* __restrict__ nwin) {
+                                               Win win) {
+  const int64_t* __restrict__ win_off = win.off;
+  int2* __restrict__ wins = win.wins;
+  int32_t* __restrict__ nwin = win.nwin;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int64_t scr[NT / 32 + 2];
   unsigned long long* bm = reinterpret_cast<unsigned long long*>(smem);
@@ -683,6 +741,11 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
         const int64_t gw0 = (wlo - lo) >> 6;
         int2* wrow = wins + win_off[row];
         const int64_t prev_last = last_id;
+        if (win.bm_save) {
+          // keep the row's bitmap for the numeric windows (no second key pass)
+          unsigned long long* dst = win.bm_save + win.bm_off[row] + gw0;
+          for (int i = threadIdx.x; i < nwords; i += NT) dst[i] = bm[i];
+        }
         __syncthreads();
         for (int i = threadIdx.x; i < nwords; i += NT) {
           const int64_t gw = gw0 + i;
@@ -707,15 +770,8 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
       }
       const int64_t base = out_off[row] + total;
       // emit sorted columns from the bitmap and clear the value slots
-      for (int i = threadIdx.x; i < nwords; i += NT) {
-        unsigned long long bits = bm[i];
-        int64_t pos = base + pre[i];
-        while (bits) {
-          const int bb = __ffsll((long long)bits) - 1;
-          bits &= bits - 1;
-          out_col[pos++] = (int32_t)(wlo + (int64_t)i * 64 + bb);
-        }
-      }
+      for (int i = threadIdx.x; i < nwords; i += NT)
+        emit_bits(bm[i], (int32_t)(wlo + (int64_t)i * 64), out_col + base + pre[i]);
       for (int64_t i = threadIdx.x; i < wtot; i += NT) out_val[base + i] = (V)0;
       __syncthreads();
       BitmapAddOp<V> ao{bm, pre, wlo, whi, out_val + base};
@@ -809,9 +865,9 @@ __device__ __forceinline__ void block_chunk_products(const Entries& E, int nent,
 
 struct WinSetOp {
   unsigned* bm32;
-  int64_t c0;
+  int32_t c0;
   __device__ __forceinline__ void operator()(int32_t col, double) {
-    const int64_t x = col - c0;
+    const uint32_t x = (uint32_t)(col - c0);
     atomicOr(bm32 + (x >> 5), 1u << (x & 31));
   }
 };
@@ -820,132 +876,326 @@ struct WinAddOp {
   const unsigned long long* bm;
   const int* pre;
   double* vals;
-  int64_t c0;
+  int32_t c0;
   __device__ __forceinline__ void operator()(int32_t col, double v) {
-    const int64_t x = col - c0;
-    const int w = (int)(x >> 6);
-    const int r = pre[w] + __popcll(bm[w] & ((1ull << (x & 63)) - 1ull));
+    const uint32_t x = (uint32_t)(col - c0);
+    const uint32_t w = x >> 6;
+    const int r = pre[w] + __popcll(bm[w] & ((2ull << (x & 63)) - 1ull)) - 1;
     smem_add(&vals[r], v);
   }
 };
 
-constexpr size_t bmw_smem() {
-  return (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8 + (size_t)3 * (WIN_NT + 1) * 8;
+// Exclusive popcount prefix over nwords <= WIN_WORDS words in one pass: each
+// lane owns up to 4 consecutive words of its warp's contiguous range.
+__device__ __forceinline__ void window_prefix(const unsigned long long* bm, int* pre, int nwords, int64_t* scr) {
+  constexpr int NW = WIN_NT / 32;
+  const int w = warp_id(), lane = lane_id();
+  const int per = (nwords + NW - 1) / NW;
+  const int L = (per + 31) / 32;  // words per lane (<= 4 for WIN_WORDS = 4096)
+  const int wb = min(nwords, per * w), we = min(nwords, per * (w + 1));
+  int c[4] = {0, 0, 0, 0};
+  int s = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = wb + lane * L + i;
+    if (i < L && idx < we) c[i] = __popcll(bm[idx]);
+    s += c[i];
+  }
+  const int inc = warp_incl_scan(s);
+  int64_t tot;
+  const int64_t wbase = block_excl_scan(lane == 31 ? (int64_t)inc : (int64_t)0, scr, &tot);
+  int run = (int)__shfl_sync(SG_FULL, wbase, 31) + inc - s;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int idx = wb + lane * L + i;
+    if (i < L && idx < we) pre[idx] = run;
+    run += c[i];
+  }
+  __syncthreads();
 }
 
+__device__ __forceinline__ void emit_bits_smem(unsigned long long bits, int32_t colbase, int* __restrict__ out) {
+  unsigned lo = (unsigned)bits, hi = (unsigned)(bits >> 32);
+  int k = 0;
+  while (lo) {
+    out[k++] = colbase + __ffs(lo) - 1;
+    lo &= lo - 1;
+  }
+  while (hi) {
+    out[k++] = colbase + 31 + __ffs(hi);
+    hi &= hi - 1;
+  }
+}
+
+#ifdef SG_PROF
+// phase cycle counters of the window kernel (profiling build only: make prof)
+__device__ unsigned long long g_phase[12];
+#define SG_PH(i)                                              \
+  if (threadIdx.x == 0) {                                     \
+    const long long _t = clock64();                           \
+    atomicAdd(&g_phase[i], (unsigned long long)(_t - _tprev)); \
+    _tprev = _t;                                              \
+  }
+#else
+#define SG_PH(i)
+#endif
+
+// position of the k-th (0-based) set bit of v
+__device__ __forceinline__ int nth_set_bit64(unsigned long long x, int k) {
+  unsigned v = (unsigned)x;
+  int pos = 0;
+  const int pl = __popc(v);
+  if (k >= pl) {
+    k -= pl;
+    v = (unsigned)(x >> 32);
+    pos = 32;
+  }
+  int p = __popc(v & 0xffffu);
+  if (k >= p) { k -= p; v >>= 16; pos += 16; }
+  p = __popc(v & 0xffu);
+  if (k >= p) { k -= p; v >>= 8; pos += 8; }
+  p = __popc(v & 0xfu);
+  if (k >= p) { k -= p; v >>= 4; pos += 4; }
+  p = __popc(v & 0x3u);
+  if (k >= p) { k -= p; v >>= 2; pos += 2; }
+  return pos + (k >= (int)(v & 1u) ? 1 : 0);
+}
+
+// A run of up to WRUN consecutive windows of one row.  Window i covers
+// columns [cb[i], cb[i+1]) and ranks [rk[i], rk[i+1]) of the row.
+constexpr int WRUN = 8;
+struct WinRun {
+  int64_t out_base;  // C index of the row's first entry
+  int64_t t0;        // A row start
+  int32_t t_len;     // A row length
+  int32_t nw;        // windows in this run
+  int32_t first;     // cb[0] is the row's first column (no lower-bound search)
+  int32_t last;      // cb[nw] is past the row's last column (no upper search)
+  int64_t bm_base;   // word offset of the row's saved bitmap (if any)
+  int32_t lo;        // the row's first output column (bitmap word 0)
+  int32_t pad;
+  int32_t cb[WRUN + 1];
+  int32_t rk[WRUN + 1];
+};
+
+constexpr size_t bmr_smem() {
+  return (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8 + (size_t)3 * (WIN_NT + 1) * 8 + (size_t)WIN_NT * 16;
+}
+
+// One CTA per run.  Rows whose A row fits one chunk keep a per-entry cursor
+// in shared memory, so window w+1 starts where window w stopped and each
+// window needs at most one lower_bound per entry (none for the last window).
 template <typename V>
-__global__ void __launch_bounds__(WIN_NT, 2) k_bmw(int64_t nwork, const int2* __restrict__ work, Csr A, Csr B,
-                                                   const int64_t* __restrict__ span_hi,
-                                                   const int64_t* __restrict__ win_off,
-                                                   const int2* __restrict__ wins, const int32_t* __restrict__ nwin,
-                                                   const int64_t* __restrict__ out_off,
+__global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinRun* __restrict__ work, Csr A, Csr B,
+                                                   const unsigned long long* __restrict__ bm_save,
                                                    int32_t* __restrict__ out_col, V* __restrict__ out_val,
                                                    unsigned long long* __restrict__ ticket) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int64_t scr[WIN_NT / 32 + 2];
-  __shared__ int64_t item;
+  __shared__ int64_t item_next;
   unsigned long long* bm = reinterpret_cast<unsigned long long*>(smem);
   int* pre = reinterpret_cast<int*>(smem + (size_t)WIN_WORDS * 8);
   double* vals = reinterpret_cast<double*>(smem + (size_t)WIN_WORDS * 12);
   unsigned char* ebase = smem + (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8;
   Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (WIN_NT + 1),
             reinterpret_cast<double*>(ebase) + 2 * (WIN_NT + 1)};
+  int64_t* cur = reinterpret_cast<int64_t*>(ebase + (size_t)3 * (WIN_NT + 1) * 8);
+  int64_t* end = cur + WIN_NT;
   const V* av = (const V*)A.val;
   const V* bv = (const V*)B.val;
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) item = (int64_t)atomicAdd(ticket, 1ull);
-    __syncthreads();
-    const int64_t b = item;
-    if (b >= nwork) return;
-    const int64_t row = work[b].x;
-    const int id = work[b].y;
-    const int2* wr = wins + win_off[row];
-    const int n = nwin[row];
-    const int2 me = wr[id];
-    if (me.x < 0) continue;
-    int64_t c1 = span_hi[row] + 1;
-    int64_t rend = out_off[row + 1] - out_off[row];
-    for (int j = id + 1; j < n; ++j) {
-      const int2 nx = wr[j];
-      if (nx.x >= 0) {
-        c1 = nx.x;
-        rend = nx.y;
-        break;
-      }
+  if (threadIdx.x == 0) item_next = (int64_t)atomicAdd(ticket, 1ull);
+  __syncthreads();
+  int64_t b = item_next;
+#ifdef SG_PROF
+  long long _tprev = clock64();
+#endif
+  while (b < nwork) {
+    const WinRun* it = work + b;
+    const int64_t t0 = it->t0;
+    const int tl = it->t_len;
+    const int nw = it->nw;
+    const int first = it->first, last = it->last;
+    const int64_t out_base = it->out_base;
+    __syncthreads();  // everyone has read item_next
+    if (threadIdx.x == 0) item_next = (int64_t)atomicAdd(ticket, 1ull);
+    const bool single = tl <= WIN_NT;
+    double my_av = 0.0;
+    if (single && (int)threadIdx.x < tl) {
+      const int32_t k = A.col[t0 + threadIdx.x];
+      int64_t s = B.ptr[k];
+      const int64_t e = B.ptr[k + 1];
+      if (!first && s < e && __ldg(B.col + s) < it->cb[0]) s = lower_bound_col(B.col, s, e, it->cb[0]);
+      cur[threadIdx.x] = s;
+      end[threadIdx.x] = e;
+      my_av = (double)av[t0 + threadIdx.x];
     }
-    const int64_t c0 = me.x;
-    const int cnt = (int)(rend - me.y);
-    const int nwords = (int)((c1 - c0 + 63) >> 6);
-    for (int i = threadIdx.x; i < nwords; i += WIN_NT) bm[i] = 0ull;
-    for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
-    __syncthreads();
-    const int64_t t0 = A.ptr[row], t1 = A.ptr[row + 1];
-    const bool single = (t1 - t0) <= WIN_NT;
-    WinSetOp so{reinterpret_cast<unsigned*>(bm), c0};
-    int nent = 0;
-    int64_t P = 0;
-    if (single) {
-      P = block_load_range<true, V>(t0, t1, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
-      block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
+    for (int w = 0; w < nw; ++w) {
+      const int32_t c0 = it->cb[w], c1 = it->cb[w + 1];
+      const int r0 = it->rk[w];
+      const int cnt = it->rk[w + 1] - r0;
+      const int nwords = (int)(((int64_t)c1 - c0 + 63) >> 6);
+      const bool saved = bm_save != nullptr;
+      if (saved) {
+        // the count pass left this row's key bitmap: copy the window's words
+        const unsigned long long* src = bm_save + it->bm_base + ((c0 - it->lo) >> 6);
+        for (int i = threadIdx.x; i < nwords; i += WIN_NT) bm[i] = src[i];
+      } else {
+        for (int i = threadIdx.x; i < nwords; i += WIN_NT) bm[i] = 0ull;
+      }
       __syncthreads();
-    } else {
-      for (int64_t t = t0; t < t1; t += WIN_NT) {
-        P = block_load_range<false, V>(t, t1, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
-        block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
+      SG_PH(0);
+      WinSetOp so{reinterpret_cast<unsigned*>(bm), c0};
+      WinAddOp ao{bm, pre, vals, c0};
+      int nent = 0;
+      int64_t P = 0;
+      if (single) {
+        int64_t s = 0, len = 0;
+        if ((int)threadIdx.x < tl) {
+          s = cur[threadIdx.x];
+          const int64_t e = end[threadIdx.x];
+          int64_t ee = e;
+          if (!(last && w == nw - 1) && s < e) {
+            if (__ldg(B.col + e - 1) >= c1) ee = (__ldg(B.col + s) >= c1) ? s : lower_bound_col(B.col, s, e, c1);
+          }
+          len = ee - s;
+          cur[threadIdx.x] = ee;
+        }
+        const int64_t S = block_excl_scan(len, scr, &P);
+        int64_t n64;
+        const int64_t pos = block_excl_scan((int64_t)(len > 0), scr, &n64);
+        if (len > 0) {
+          E.S[pos] = S;
+          E.bs[pos] = s;
+          E.av[pos] = my_av;
+        }
         __syncthreads();
+        nent = (int)n64;
+        SG_PH(1);
+#ifdef SG_PROF
+        if (threadIdx.x == 0) atomicAdd(&g_phase[8], (unsigned long long)P);
+#endif
+        if (!saved) {
+          block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
+          __syncthreads();
+        }
+      } else if (!saved) {
+        for (int64_t t = t0; t < t0 + tl; t += WIN_NT) {
+          P = block_load_range<false, V>(t, t0 + tl, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
+          block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
+          __syncthreads();
+        }
       }
-    }
-    bitmap_prefix<WIN_NT>(bm, pre, nwords, scr);
-    WinAddOp ao{bm, pre, vals, c0};
-    if (single) {
-      block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
+      SG_PH(2);
+      window_prefix(bm, pre, nwords, scr);
+      // columns first: expand the bitmap into a staging array that overlays
+      // the (not yet used) value slots, then copy it out coalesced
+      const int64_t base = out_base + r0;
+      int* colbuf = reinterpret_cast<int*>(vals);
+      for (int i = threadIdx.x; i < nwords; i += WIN_NT) emit_bits_smem(bm[i], c0 + 64 * i, colbuf + pre[i]);
       __syncthreads();
-    } else {
-      for (int64_t t = t0; t < t1; t += WIN_NT) {
-        P = block_load_range<true, V>(t, t1, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
+      for (int i = threadIdx.x; i < cnt; i += WIN_NT) out_col[base + i] = colbuf[i];
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
+      __syncthreads();
+      SG_PH(3);
+      if (single) {
         block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
         __syncthreads();
+      } else {
+        for (int64_t t = t0; t < t0 + tl; t += WIN_NT) {
+          P = block_load_range<true, V>(t, t0 + tl, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
+          block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
+          __syncthreads();
+        }
       }
-    }
-    const int64_t base = out_off[row] + me.y;
-    for (int i = threadIdx.x; i < nwords; i += WIN_NT) {
-      unsigned long long bits = bm[i];
-      int64_t pos = base + pre[i];
-      while (bits) {
-        const int bb = __ffsll((long long)bits) - 1;
-        bits &= bits - 1;
-        out_col[pos++] = (int32_t)(c0 + (int64_t)i * 64 + bb);
+      SG_PH(4);
+      for (int i = threadIdx.x; i < cnt; i += WIN_NT) out_val[base + i] = (V)vals[i];
+      __syncthreads();
+      SG_PH(5);
+#ifdef SG_PROF
+      if (threadIdx.x == 0) {
+        atomicAdd(&g_phase[9], 1ull);
+        atomicAdd(&g_phase[10], (unsigned long long)nwords);
+        atomicAdd(&g_phase[11], (unsigned long long)cnt);
       }
+#endif
     }
-    for (int i = threadIdx.x; i < cnt; i += WIN_NT) out_val[base + i] = (V)vals[i];
-    __syncthreads();
+    b = item_next;
   }
 }
 
-// work list: (row, window id) for every row with windows
-__global__ void k_win_counts(int64_t m, const int32_t* __restrict__ nwin, int64_t* __restrict__ n_out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < m) n_out[i] = nwin[i] > 0 ? nwin[i] : 0;
-}
-
-__global__ void k_win_scatter(int64_t m, const int32_t* __restrict__ nwin, const int64_t* __restrict__ off,
-                              int2* __restrict__ work) {
+// runs per row (used windows / WRUN, rounded up)
+__global__ void k_win_counts(int64_t m, const int64_t* __restrict__ win_off, const int2* __restrict__ wins,
+                             const int32_t* __restrict__ nwin, int64_t* __restrict__ n_out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int n = nwin[i];
-  const int64_t o = off[i];
-  for (int j = 0; j < n; ++j) work[o + j] = make_int2((int)i, j);
+  int c = 0;
+  if (n > 0) {
+    const int2* wr = wins + win_off[i];
+    for (int j = 0; j < n; ++j) c += wr[j].x >= 0;
+  }
+  n_out[i] = (c + WRUN - 1) / WRUN;
+}
+
+__global__ void k_win_scatter(int64_t m, const int64_t* __restrict__ a_ptr, const int64_t* __restrict__ span_lo,
+                              const int64_t* __restrict__ span_hi, const int64_t* __restrict__ win_off,
+                              const int2* __restrict__ wins, const int32_t* __restrict__ nwin,
+                              const int64_t* __restrict__ out_off, const int64_t* __restrict__ off,
+                              const int64_t* __restrict__ bm_off, WinRun* __restrict__ work) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int n = nwin[i];
+  if (n <= 0) return;
+  const int2* wr = wins + win_off[i];
+  int64_t o = off[i];
+  const int32_t rowcnt = (int32_t)(out_off[i + 1] - out_off[i]);
+  const int32_t hi1 = (int32_t)(span_hi[i] + 1);
+  WinRun run;
+  run.out_base = out_off[i];
+  run.bm_base = bm_off ? bm_off[i] : 0;
+  run.lo = (int32_t)span_lo[i];
+  run.pad = 0;
+  run.t0 = a_ptr[i];
+  run.t_len = (int32_t)(a_ptr[i + 1] - a_ptr[i]);
+  run.nw = 0;
+  run.first = 1;
+  for (int j = 0; j <= n; ++j) {
+    const bool at_end = j == n;
+    if (!at_end && wr[j].x < 0) continue;
+    const int32_t c = at_end ? hi1 : wr[j].x;
+    const int32_t r = at_end ? rowcnt : wr[j].y;
+    if (run.nw == WRUN || at_end) {
+      // close the run at boundary (c, r)
+      if (run.nw > 0) {
+        run.cb[run.nw] = c;
+        run.rk[run.nw] = r;
+        run.last = at_end ? 1 : 0;
+        work[o++] = run;
+        run.first = 0;
+        run.nw = 0;
+      }
+    }
+    if (!at_end) {
+      run.cb[run.nw] = c;
+      run.rk[run.nw] = r;
+      run.nw++;
+    }
+  }
 }
 
 __global__ void k_win_capacity(int64_t m, const int64_t* __restrict__ products, const int64_t* __restrict__ lo,
                                const int64_t* __restrict__ hi, const uint8_t* __restrict__ select,
-                               int64_t* __restrict__ cap) {
+                               int64_t* __restrict__ cap, int64_t* __restrict__ words) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int64_t p = products[i];
-  const bool sel = (select == nullptr || select[i]) && p > 256;
-  cap[i] = sel ? window_capacity(p, hi[i] - lo[i] + 1) : 0;
+  const int64_t span = hi[i] - lo[i] + 1;
+  // symbolic pass: only rows the count classifier sends to a bitmap kernel;
+  // fallback count pass (select given): every selected long row
+  const bool sel = select == nullptr ? count_uses_bitmap(p, span) : (select[i] && p > 256);
+  cap[i] = sel ? window_capacity(p, span) : 0;
+  if (words) words[i] = sel ? (span + 63) / 64 : 0;
 }
 
 // -------------------------------------------------------------------------
@@ -989,14 +1239,12 @@ __global__ void k_classify_count(int64_t m, const int64_t* __restrict__ products
   } else {
     const int64_t span = hi[i] - lo[i] + 1;
     const int64_t T = max(pow2_at_least(2 * p), (int64_t)32);
-    if (p <= 1024) {
+    if (count_uses_bitmap(p, span)) {
+      b = bm_bin(span);
+    } else if (p <= 1024) {
       b = (uint8_t)(BIN_HW0 + log2_pow2(T) - 5);
-    } else if (span <= ((int64_t)1 << 20) && (span + 63) / 64 <= p) {
-      b = bm_bin(span);
-    } else if (T <= 32768) {
-      b = (uint8_t)(BIN_HB0 + log2_pow2(max(T, (int64_t)4096)) - 12);
     } else {
-      b = bm_bin(span);
+      b = (uint8_t)(BIN_HB0 + log2_pow2(max(T, (int64_t)4096)) - 12);
     }
   }
   bins[i] = b;
@@ -1088,9 +1336,7 @@ struct Launch {
   int64_t* counts;
   uint8_t* overflow;
   cudaStream_t s;
-  const int64_t* win_off = nullptr;  // count mode: emit numeric windows
-  int2* wins = nullptr;
-  int32_t* nwin = nullptr;
+  Win win{nullptr, nullptr, nullptr, nullptr, nullptr};  // count mode: record numeric windows
 };
 
 template <int LOG2T, int MODE, typename V>
@@ -1121,8 +1367,8 @@ static int launch_bm(const Launch& L, const int32_t* rows, int64_t n) {
   if (int rc = set_smem(kern, sm)) return rc;
   int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 32);
   kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.lo, L.hi, L.out_off, L.out_col,
-                           (V*)L.out_val, L.counts, L.overflow, MODE == 0 ? L.win_off : nullptr,
-                           MODE == 0 ? L.wins : nullptr, MODE == 0 ? L.nwin : nullptr);
+                           (V*)L.out_val, L.counts, L.overflow,
+                           MODE == 0 ? L.win : Win{nullptr, nullptr, nullptr, nullptr, nullptr});
   return check_cuda("k_bitmap");
 }
 
@@ -1190,10 +1436,15 @@ using namespace sg;
 
 extern "C" {
 
+static Win to_win(const sg_windows_t* w) {
+  if (!w) return Win{nullptr, nullptr, nullptr, nullptr, nullptr};
+  return Win{w->win_off, reinterpret_cast<int2*>(w->wins), w->nwin, w->bm_off,
+             reinterpret_cast<unsigned long long*>(w->bm_save)};
+}
+
 int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col, const int64_t* b_ptr,
                 const int32_t* b_col, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
-                int64_t* counts, const int64_t* win_off, int32_t* wins, int32_t* nwin, void* ws,
-                size_t ws_bytes, void* stream) {
+                int64_t* counts, const sg_windows_t* win, void* ws, size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   if (m == 0) return SG_OK;
@@ -1202,9 +1453,7 @@ int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t*
   if (int rc = check_cuda("k_classify_count")) return rc;
   Launch L{{a_ptr, a_col, nullptr}, {b_ptr, b_col, nullptr}, nullptr, nullptr, nullptr, span_lo, span_hi,
            nullptr, nullptr, nullptr, counts, nullptr, s};
-  L.win_off = win_off;
-  L.wins = reinterpret_cast<int2*>(wins);
-  L.nwin = nwin;
+  L.win = to_win(win);
   (void)b_ncols;
   return run_bins<0, double>(L, m, w, nullptr);
 }
@@ -1235,7 +1484,7 @@ int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, i
                 const int32_t* a_col, const void* a_val, const int64_t* b_ptr, const int32_t* b_col,
                 const void* b_val, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
                 const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts,
-                const int64_t* win_off, int32_t* wins, int32_t* nwin, void* ws, size_t ws_bytes, void* stream) {
+                const sg_windows_t* win, void* ws, size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, nrows, w)) return SG_ERR_WORKSPACE;
   if (nrows == 0) return SG_OK;
@@ -1252,11 +1501,7 @@ int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, i
   if (int rc = check_cuda("k_gather_rows")) return rc;
   Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, nullptr, nullptr, nullptr, span_lo, span_hi,
            out_off, out_col, out_val, counts, nullptr, s};
-  if (mode == 0) {
-    L.win_off = win_off;
-    L.wins = reinterpret_cast<int2*>(wins);
-    L.nwin = nwin;
-  }
+  if (mode == 0) L.win = to_win(win);
   for (int b : kOrder) {
     if (cnt[b] == 0) continue;
     int rc;
@@ -1272,31 +1517,37 @@ int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, i
 }
 
 int sg_window_capacity(int64_t m, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
-                       const uint8_t* select, int64_t* win_off, int64_t* total_host, void* ws, size_t ws_bytes,
-                       void* stream) {
+                       const uint8_t* select, int64_t* win_off, int64_t* bm_off, int64_t* totals_host, void* ws,
+                       size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
+  // capacities into win_off[0..m) and word counts into bm_off[0..m), then
+  // both are scanned in place (the scan reads each tile before writing it)
   if (m > 0) {
-    k_win_capacity<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, select, w.tmp);
+    k_win_capacity<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, select, win_off, bm_off);
     if (int rc = check_cuda("k_win_capacity")) return rc;
   }
-  if (int rc = scan_i64(m, w.tmp, win_off, w.partials, s)) return rc;
-  cudaMemcpyAsync(total_host, win_off + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (int rc = scan_i64(m, win_off, win_off, w.partials, s)) return rc;
+  if (bm_off)
+    if (int rc = scan_i64(m, bm_off, bm_off, w.partials, s)) return rc;
+  cudaMemcpyAsync(totals_host, win_off + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (bm_off) cudaMemcpyAsync(totals_host + 1, bm_off + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_capacity sync", 0);
+  if (!bm_off) totals_host[1] = 0;
   return SG_OK;
 }
 
 int sg_window_numeric(int64_t m, int dtype, const int64_t* a_ptr, const int32_t* a_col, const void* a_val,
-                      const int64_t* b_ptr, const int32_t* b_col, const void* b_val, const int64_t* span_hi,
-                      const int64_t* win_off, const int32_t* wins, const int32_t* nwin, const int64_t* out_off,
-                      int32_t* out_col, void* out_val, int32_t* work_buf, int64_t work_cap, void* ws,
-                      size_t ws_bytes, void* stream) {
+                      const int64_t* b_ptr, const int32_t* b_col, const void* b_val, const int64_t* span_lo,
+                      const int64_t* span_hi, const sg_windows_t* win, const int64_t* out_off, int32_t* out_col,
+                      void* out_val, void* work_buf, int64_t work_cap, void* ws, size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
-  if (m == 0) return SG_OK;
+  if (m == 0 || win == nullptr) return SG_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  k_win_counts<<<grid_for(m, 256), 256, 0, s>>>(m, nwin, w.tmp);
+  const Win W = to_win(win);
+  k_win_counts<<<grid_for(m, 256), 256, 0, s>>>(m, W.off, W.wins, W.nwin, w.tmp);
   if (int rc = check_cuda("k_win_counts")) return rc;
   if (int rc = scan_i64(m, w.tmp, w.tmp, w.partials, s)) return rc;
   int64_t nwork = 0;
@@ -1307,27 +1558,34 @@ int sg_window_numeric(int64_t m, int dtype, const int64_t* a_ptr, const int32_t*
     set_error("sg_window_numeric: work buffer too small");
     return SG_ERR_WORKSPACE;
   }
-  int2* work = reinterpret_cast<int2*>(work_buf);
-  k_win_scatter<<<grid_for(m, 256), 256, 0, s>>>(m, nwin, w.tmp, work);
+  WinRun* work = reinterpret_cast<WinRun*>(work_buf);
+  k_win_scatter<<<grid_for(m, 256), 256, 0, s>>>(m, a_ptr, span_lo, span_hi, W.off, W.wins, W.nwin, out_off,
+                                                 w.tmp, W.bm_save ? W.bm_off : nullptr, work);
   if (int rc = check_cuda("k_win_scatter")) return rc;
   unsigned long long* ticket = reinterpret_cast<unsigned long long*>(w.bincnt);
   cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s);
-  constexpr size_t sm = bmw_smem();
+  constexpr size_t sm = bmr_smem();
   const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
-  const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms() * 2);
-  const int2* wn = reinterpret_cast<const int2*>(wins);
+  const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms());
   if (dtype == SG_F64) {
-    auto kern = k_bmw<double>;
+    auto kern = k_bmr<double>;
     if (int rc = set_smem(kern, sm)) return rc;
-    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, span_hi, win_off, wn, nwin, out_off, out_col,
-                                  (double*)out_val, ticket);
+    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, W.bm_save, out_col, (double*)out_val, ticket);
   } else {
-    auto kern = k_bmw<float>;
+    auto kern = k_bmr<float>;
     if (int rc = set_smem(kern, sm)) return rc;
-    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, span_hi, win_off, wn, nwin, out_off, out_col,
-                                  (float*)out_val, ticket);
+    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, W.bm_save, out_col, (float*)out_val, ticket);
   }
-  return check_cuda("k_bmw");
+  return check_cuda("k_bmr");
 }
+
+#ifdef SG_PROF
+int sg_debug_phase_cycles(unsigned long long* out12) {
+  cudaMemcpyFromSymbol(out12, g_phase, sizeof(unsigned long long) * 12);
+  unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+  return check_cuda("sg_debug_phase_cycles", 0);
+}
+#endif
 
 }  // extern "C"

@@ -21,7 +21,7 @@ Memory layout differences (results are identical):
 
 from __future__ import annotations
 
-import math
+import ctypes
 import time
 from dataclasses import replace
 
@@ -142,25 +142,63 @@ def scan(ctx: _Ctx, x):
 
 
 class Windows:
-    """Numeric window table of the long rows (see include/sgb200.h)."""
+    """Numeric window tables of the long rows (sg_windows_t, include/sgb200.h)."""
 
-    def __init__(self, off, wins, nwin, total):
-        self.off, self.wins, self.nwin, self.total = off, wins, nwin, total
+    def __init__(self, off, wins, nwin, bm_off, bm_save, total):
+        self.off, self.wins, self.nwin, self.bm_off, self.bm_save, self.total = off, wins, nwin, bm_off, bm_save, total
+        self._struct = None
 
-    def args(self):
-        return ptr(self.off), ptr(self.wins), ptr(self.nwin)
+    def struct(self):
+        s = _lib.SgWindows()
+        s.win_off, s.wins, s.nwin = ptr(self.off), ptr(self.wins), ptr(self.nwin)
+        s.bm_off = ptr(self.bm_off) if self.bm_save is not None else None
+        s.bm_save = ptr(self.bm_save) if self.bm_save is not None else None
+        self._struct = s  # keep alive for the call
+        return s
+
+    def drop_bitmaps(self):
+        """Release the saved key bitmaps (the window pass then rebuilds keys)."""
+        self.bm_save = None
+
+
+# saved key bitmaps may use at most this share of the free device memory
+BITMAP_SAVE_SHARE = 0.35
 
 
 def windows(ctx: _Ctx, m, products, lo, hi, select) -> Windows:
     off = ctx.empty(m + 1, torch.int64)
-    total = ctypes_int64()
+    bm_off = ctx.empty(m + 1, torch.int64)
+    totals = (ctypes.c_int64 * 2)()
     ws, wsb = ctx.workspace(max(m, 1))
-    _lib.call("sg_window_capacity", m, ptr(products), ptr(lo), ptr(hi), ptr(select), ptr(off), total,
-              ws, wsb, ctx.sp)
-    total = int(total.value)
+    _lib.call("sg_window_capacity", m, ptr(products), ptr(lo), ptr(hi), ptr(select), ptr(off), ptr(bm_off),
+              ctypes.cast(totals, ctypes.c_void_p), ws, wsb, ctx.sp)
+    total, words = int(totals[0]), int(totals[1])
     wins = torch.full((max(2 * total, 2),), -1, dtype=torch.int32, device=ctx.device)
     nwin = torch.zeros(max(m, 1), dtype=torch.int32, device=ctx.device)
-    return Windows(off, wins, nwin, total)
+    bm_save = None
+    if total and words:
+        free, _ = torch.cuda.mem_get_info(ctx.device)
+        # blocks cached by torch's allocator are free for this purpose too
+        free += torch.cuda.memory_reserved(ctx.device) - torch.cuda.memory_allocated(ctx.device)
+        if 8 * words <= BITMAP_SAVE_SHARE * free:
+            try:
+                bm_save = torch.empty(words, dtype=torch.int64, device=ctx.device)
+            except torch.OutOfMemoryError:
+                bm_save = None
+    return Windows(off, wins, nwin, bm_off, bm_save, total)
+
+
+def alloc_c(ctx: _Ctx, nnz, dtype, win):
+    """C's column / value arrays; if they do not fit next to the saved key
+    bitmaps, the bitmaps are released (the window pass rebuilds keys)."""
+    try:
+        return ctx.empty(nnz, torch.int32), ctx.empty(nnz, dtype)
+    except ResourceLimitError:
+        if win is None or win.bm_save is None:
+            raise
+        win.drop_bitmaps()
+        torch.cuda.empty_cache()
+        return ctx.empty(nnz, torch.int32), ctx.empty(nnz, dtype)
 
 
 def select_fallback(ctx: _Ctx, m, kind, products, overflow, exclude):
@@ -270,7 +308,7 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         pred = ctx.empty(m, torch.int64)
         win = windows(ctx, m, products, span_lo, span_hi, None)
         _lib.call("sg_symbolic", m, n, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
-                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(pred), *win.args(), ws, wsb, ctx.sp)
+                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(pred), win.struct(), ws, wsb, ctx.sp)
         pred_kind = "exact"
     elif kind_wf is WorkflowKind.HLL_ESTIMATION:
         pred = hll_estimate(ctx, A, regs, p)
@@ -308,8 +346,7 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     if exact:
         row_ptr = scan(ctx, pred)
         nnz_c = int(row_ptr[-1].item()) if m else 0
-        out_col = ctx.empty(nnz_c, torch.int32)
-        out_val = ctx.empty(nnz_c, dtype)
+        out_col, out_val = alloc_c(ctx, nnz_c, dtype, win)
         out_off = row_ptr
     else:
         main_alloc = torch.where(kind == int(PlanKind.FALLBACK), torch.zeros_like(alloc), alloc)
@@ -339,19 +376,18 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         win = windows(ctx, m, products, span_lo, span_hi, sel)
         if n_fb:
             _lib.call("sg_fallback", 0, n_fb, ptr(fb_rows), n, dcode, *fargs, None, None, None,
-                      ptr(counts), *win.args(), ws, wsb, ctx.sp)
+                      ptr(counts), win.struct(), ws, wsb, ctx.sp)
         row_ptr = scan(ctx, counts)
         nnz_c = int(row_ptr[-1].item()) if m else 0
-        C_col = ctx.empty(nnz_c, torch.int32)
-        C_val = ctx.empty(nnz_c, dtype)
+        C_col, C_val = alloc_c(ctx, nnz_c, dtype, win)
     if win is not None and win.total:
-        work = ctx.empty(2 * win.total, torch.int32)
-        _lib.call("sg_window_numeric", m, dcode, *Aargs, ptr(span_hi), *win.args(), ptr(row_ptr),
+        work = ctx.empty(15 * win.total, torch.int64)  # <= one 120-byte run per window
+        _lib.call("sg_window_numeric", m, dcode, *Aargs, ptr(span_lo), ptr(span_hi), win.struct(), ptr(row_ptr),
                   ptr(C_col), ptr(C_val), ptr(work), win.total, ws, wsb, ctx.sp)
     rest, n_rest = (fb_rows, n_fb) if win is None else select_fallback(ctx, m, kind, products, overflow, win.nwin)
     if n_rest:
         _lib.call("sg_fallback", 1, n_rest, ptr(rest), n, dcode, *fargs, ptr(row_ptr),
-                  ptr(C_col), ptr(C_val), ptr(counts), None, None, None, ws, wsb, ctx.sp)
+                  ptr(C_col), ptr(C_val), ptr(counts), None, ws, wsb, ctx.sp)
     ev[5].record(ctx.stream)
     ctx.sync()
     t5 = time.perf_counter()

@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_bmr -c 1 -o gpurun_out/prof_bmr python tools/run_once.py rmat17 > gpurun_out/prof_bmr.log 2>&1
+ls -la gpurun_out/prof_bmr.ncu-rep

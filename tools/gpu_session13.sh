@@ -1,0 +1,2 @@
+#!/bin/bash
+SGB200_LIB=paper_2604_19004_b200/libsgb200_prof.so timeout 600 python tools/phase_prof.py rmat18 2>&1 | tail -11
