@@ -27,6 +27,8 @@
 // B row keeps all warps busy.
 #include <algorithm>
 #include <climits>
+
+#include <cub/block/block_radix_sort.cuh>
 #include <string>
 
 #include "sg_internal.cuh"
@@ -89,18 +91,20 @@ __device__ __forceinline__ void warp_products(const Entries& E, int nent, int64_
     if (seg_end >= blk_end) {
       const int64_t base = E.bs[c0] + (p0 - E.S[c0]) + lane;
       const double a = VALUES ? E.av[c0] : 0.0;
-      const int64_t nvalid = blk_end - p0;
+      const int nvalid = (int)(blk_end - p0) - lane;  // lanes with products in step u: 32u < nvalid
+      const int32_t* cp = b_col + base;
+      const V* vp = b_val + base;
       int32_t col[UNR];
       double bv[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        const bool ok = 32 * u + lane < nvalid;
-        col[u] = ok ? __ldg(b_col + base + 32 * u) : 0;
-        bv[u] = (VALUES && ok) ? (double)__ldg(b_val + base + 32 * u) : 0.0;
+        const bool ok = 32 * u < nvalid;
+        col[u] = ok ? __ldg(cp + 32 * u) : 0;
+        bv[u] = (VALUES && ok) ? (double)__ldg(vp + 32 * u) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < UNR; ++u)
-        if (32 * u + lane < nvalid) op(col[u], VALUES ? a * bv[u] : 0.0);
+        if (32 * u < nvalid) op(col[u], VALUES ? a * bv[u] : 0.0);
       if (seg_end == blk_end) ++c0;
       if (c0 >= nent) c0 = nent - 1;
       continue;
@@ -397,6 +401,8 @@ constexpr size_t hw_smem() {
 template <int LOG2T, int MODE, typename V, int NT>
 __global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* __restrict__ rows, Csr A, Csr B,
                                                    const int8_t* kind, const int64_t* cap, const int64_t* alloc,
+                                                   const int64_t* __restrict__ span_lo,
+                                                   const int64_t* __restrict__ span_hi,
                                                    const int64_t* __restrict__ out_off,
                                                    int32_t* __restrict__ out_col, V* __restrict__ out_val,
                                                    int64_t* __restrict__ counts, uint8_t* __restrict__ overflow) {
@@ -451,14 +457,35 @@ __global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* 
       n += tot;
       __syncthreads();
     }
-    const int pad = (int)next_pow2_u32((uint32_t)max((int)n, 1));
-    for (int i = (int)n + threadIdx.x; i < pad; i += NT) keys[i] = INT_MAX;
-    __syncthreads();
-    bitonic_kv(keys, vals, pad, threadIdx.x, NT, BlockSync{});
-    const int64_t off = out_off[row];
-    for (int i = threadIdx.x; i < n; i += NT) {
-      out_col[off + i] = keys[i];
-      out_val[off + i] = (V)vals[i];
+    // sort the n <= T/2 distinct columns: LSD radix sort (CUB block
+    // primitive) on (col - span_lo) over only the bits the row's span needs,
+    // values carried along; striped output -> coalesced stores
+    {
+      constexpr int ITEMS = (T / 2) / NT;
+      using Sorter = cub::BlockRadixSort<uint32_t, NT, ITEMS, double>;
+      const int32_t lo32 = (int32_t)span_lo[row];
+      const uint32_t span = (uint32_t)(span_hi[row] - span_lo[row] + 1);
+      const int bits = span <= 1 ? 1 : 32 - __clz(span - 1);
+      uint32_t kk[ITEMS];
+      double vv[ITEMS];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int idx = threadIdx.x * ITEMS + i;
+        kk[i] = idx < n ? (uint32_t)(keys[idx] - lo32) : 0xffffffffu;
+        vv[i] = idx < n ? vals[idx] : 0.0;
+      }
+      __syncthreads();
+      auto& tmp = *reinterpret_cast<typename Sorter::TempStorage*>(smem);
+      Sorter(tmp).SortBlockedToStriped(kk, vv, 0, bits < 32 ? bits + 1 : 32);
+      const int64_t off = out_off[row];
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int idx = i * NT + threadIdx.x;
+        if (idx < n) {
+          out_col[off + idx] = (int32_t)kk[i] + lo32;
+          out_val[off + idx] = (V)vv[i];
+        }
+      }
     }
     if (threadIdx.x == 0) {
       counts[row] = n;
@@ -564,10 +591,11 @@ __global__ void __launch_bounds__(ESC_WARPS * 32) k_esc(int64_t nbin, const int3
 template <typename V>
 struct BitmapSetOp {
   unsigned long long* bm;
-  int64_t wlo, whi;
+  int32_t wlo;
+  uint32_t wspan;  // whi - wlo
   __device__ __forceinline__ void operator()(int32_t col, double) {
-    if (col < wlo || col > whi) return;
-    const int64_t x = col - wlo;
+    const uint32_t x = (uint32_t)(col - wlo);
+    if (x > wspan) return;
     // 32-bit ATOMS.OR is native on sm_100a (the 64-bit form is a CAS loop)
     atomicOr(reinterpret_cast<unsigned*>(bm) + (x >> 5), 1u << (x & 31));
   }
@@ -699,7 +727,7 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
         const int nwords = (int)((whi - wlo) / 64 + 1);
         for (int i = threadIdx.x; i < nwords; i += NT) bm[i] = 0ull;
         __syncthreads();
-        BitmapSetOp<V> so{bm, wlo, whi};
+        BitmapSetOp<V> so{bm, (int32_t)wlo, (uint32_t)(whi - wlo)};
         block_row<false, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, so,
                             nullptr);
         int64_t c = 0;
@@ -724,7 +752,7 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
       const int nwords = (int)((whi - wlo) / 64 + 1);
       for (int i = threadIdx.x; i < nwords; i += NT) bm[i] = 0ull;
       __syncthreads();
-      BitmapSetOp<V> so{bm, wlo, whi};
+      BitmapSetOp<V> so{bm, (int32_t)wlo, (uint32_t)(whi - wlo)};
       block_row<false, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, so, nullptr);
       if (MODE == 0 && wcap == 0) {
         int64_t c = 0;
@@ -747,17 +775,18 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
           for (int i = threadIdx.x; i < nwords; i += NT) dst[i] = bm[i];
         }
         __syncthreads();
+        const uint32_t tot32 = (uint32_t)total;
         for (int i = threadIdx.x; i < nwords; i += NT) {
-          const int64_t gw = gw0 + i;
-          const int64_t rank = total + pre[i];
-          const int64_t id = rank / WIN_RP + gw / WIN_WORDS;
+          const uint32_t gw = (uint32_t)gw0 + (uint32_t)i;
+          const uint32_t rank = tot32 + (uint32_t)pre[i];
+          const int64_t id = (int64_t)(rank / (uint32_t)WIN_RP + gw / (uint32_t)WIN_WORDS);
           int64_t idp = -1;
           if (i > 0) {
-            idp = (total + pre[i - 1]) / WIN_RP + (gw - 1) / WIN_WORDS;
+            idp = (int64_t)((tot32 + (uint32_t)pre[i - 1]) / (uint32_t)WIN_RP + (gw - 1) / (uint32_t)WIN_WORDS);
           } else if (gw > 0) {
             idp = prev_last;
           }
-          if (id != idp && id < wcap) wrow[id] = make_int2((int)(lo + 64 * gw), (int)rank);
+          if (id != idp && id < wcap) wrow[id] = make_int2((int)(lo + 64 * (int64_t)gw), (int)rank);
           if (i == nwords - 1) last_id = id;
         }
         total += wtot;
@@ -1355,8 +1384,8 @@ static int launch_hb(const Launch& L, const int32_t* rows, int64_t n) {
   auto kern = k_hash_block<LOG2T, MODE, V, NT>;
   if (int rc = set_smem(kern, sm)) return rc;
   int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 16);
-  kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.out_off, L.out_col, (V*)L.out_val,
-                           L.counts, L.overflow);
+  kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.lo, L.hi, L.out_off, L.out_col,
+                           (V*)L.out_val, L.counts, L.overflow);
   return check_cuda("k_hash_block");
 }
 
