@@ -215,21 +215,29 @@ def main():
     same = b is a
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     vbytes = 8 if args.dtype == "f64" else 4
-    # shard rows by balanced products (north star: row-sharded, B replicated)
-    per = row_products(a, b)
-    cum = np.r_[0, np.cumsum(per)]
-    total_products = int(cum[-1])
-    cuts = [int(np.searchsorted(cum, total_products * r / n_gpus, side="left")) for r in range(n_gpus + 1)]
-    cuts[0], cuts[-1] = 0, a.nrows
-    lo, hi = cuts[rank], cuts[rank + 1]
-    a_loc = rows_slice(a, lo, hi) if n_gpus > 1 else a
-    A = to_device(a_loc, dev, dt)
-    B = to_device(b, dev, dt) if (not same or n_gpus > 1) else A
     cfg = EngineConfig(return_device=True, dtype=args.dtype)
-    torch.cuda.synchronize()
+    if n_gpus == 1:
+        a_loc = a
+        A = to_device(a, dev, dt)
+        B = A if same else to_device(b, dev, dt)
 
-    def step():
-        return spgemm(A, B if not (same and n_gpus == 1) else A, cfg)
+        def step():
+            return spgemm(A, B, cfg)
+    else:
+        # row-sharded job (shard.py): every step broadcasts B from rank 0
+        # over NCCL, cuts A's rows by balanced products (row-stats kernel on
+        # rank 0), multiplies the local rows, and exchanges nnz offsets
+        from paper_2604_19004_b200.shard import gpu_local_fn, gpu_products_fn, spgemm_sharded
+        A0 = to_device(a, dev, dt) if rank == 0 else None
+        B0 = (A0 if same else to_device(b, dev, dt)) if rank == 0 else None
+        local_fn = gpu_local_fn(cfg)
+
+        def step():
+            sh = spgemm_sharded(A0, B0, local_fn, device=dev, gather=False, products_fn=gpu_products_fn(dev))
+            return sh, sh.report
+
+        a_loc = None
+    torch.cuda.synchronize()
 
     c = rep = None
     for _ in range(args.warmup):
@@ -275,7 +283,9 @@ def main():
     # roofline of the dominant stage on this rank (CUDA events on the launch stream)
     peak, peak_kind = load_peaks()
     m, k = a.nrows, b.nrows
-    alg = compulsory_bytes(a_loc.nrows, k, a_loc.nnz, prod_loc, nnz_c_loc, vbytes)
+    loc_rows = rep.nrows_local if hasattr(rep, "nrows_local") else (a_loc.nrows if a_loc is not None else m // n_gpus)
+    loc_nnz = a_loc.nnz if a_loc is not None else a.nnz // n_gpus
+    alg = compulsory_bytes(loc_rows, k, loc_nnz, prod_loc, nnz_c_loc, vbytes)
     per_step = {kk: v / args.steps for kk, v in stage_ms.items() if kk != "h2d"}
     dom = max(per_step, key=per_step.get) if per_step else "numeric"
     num_ms = per_step.get("numeric", 0.0) + per_step.get("fallback", 0.0) + per_step.get("compact", 0.0)
@@ -288,21 +298,32 @@ def main():
     if not args.no_e2e:
         try:
             cfg_h = EngineConfig(dtype=args.dtype)
-            a_h = a_loc if args.dtype == "f64" else a_loc.astype(np.float32)
-            b_h = (a_h if (same and n_gpus == 1) else (b if args.dtype == "f64" else b.astype(np.float32)))
+            a_h = a if args.dtype == "f64" else a.astype(np.float32)
+            b_h = (a_h if same else (b if args.dtype == "f64" else b.astype(np.float32)))
             ts = []
             cbytes = 0
             for _ in range(max(1, args.e2e_steps)):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                ch, rh = spgemm(a_h, b_h, cfg_h)
+                if n_gpus == 1:
+                    ch, rh = spgemm(a_h, b_h, cfg_h)
+                    cbytes = ch.row_ptr.nbytes + ch.col_idx.nbytes + ch.values.nbytes
+                else:
+                    from paper_2604_19004_b200.device import download
+                    from paper_2604_19004_b200.shard import gpu_local_fn, gpu_products_fn, spgemm_sharded
+                    sh = spgemm_sharded(a_h if rank == 0 else None, b_h if rank == 0 else None,
+                                        gpu_local_fn(cfg), device=dev, gather=False,
+                                        products_fn=gpu_products_fn(dev))
+                    ch = [download(sh.row_ptr), download(sh.col_idx), download(sh.values)]
+                    cbytes = sum(x.nbytes for x in ch)
                 torch.cuda.synchronize()
                 ts.append(time.perf_counter() - t0)
-                cbytes = ch.row_ptr.nbytes + ch.col_idx.nbytes + ch.values.nbytes
                 del ch
             h2d = a_h.row_ptr.nbytes + a_h.col_idx.nbytes + a_h.values.nbytes
             if b_h is not a_h:
                 h2d += b_h.row_ptr.nbytes + b_h.col_idx.nbytes + b_h.values.nbytes
+            if n_gpus > 1 and rank != 0:
+                h2d = 0  # only the root uploads; the others receive over NVLink
             tw = torch.tensor([max(ts) if world > 1 else float(np.mean(ts))], dtype=torch.float64, device=dev)
             if world > 1:
                 dist.all_reduce(tw, op=dist.ReduceOp.MAX)

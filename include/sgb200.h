@@ -99,6 +99,9 @@ int sg_hll_estimate(int64_t nsel, const int64_t* rows, const int64_t* a_ptr,
  *  bm_off   int64[m+1]  word offsets of saved key bitmaps, or NULL
  *  bm_save  uint64[bm_off[m]] saved key bitmaps, or NULL (then the numeric
  *           pass rebuilds each window's key bitmap from the products)
+ *  pre_save int32[bm_off[m]] row-relative rank at each saved word (with
+ *           bm_save; lets the numeric pass skip the prefix and write C's
+ *           columns with a separate streaming expansion)
  * Each window holds at most 16384 distinct columns over at most 262144
  * columns, so its bitmap, rank prefix and values sit in shared memory. */
 typedef struct sg_windows {
@@ -107,6 +110,7 @@ typedef struct sg_windows {
   int32_t* nwin;
   const int64_t* bm_off;
   uint64_t* bm_save;
+  int32_t* pre_save;
 } sg_windows_t;
 
 /* Sizes the window tables for rows with select[row] != 0 (all rows when

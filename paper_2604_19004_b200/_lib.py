@@ -23,7 +23,7 @@ I64, I32, SZ, P, D = C.c_int64, C.c_int, C.c_size_t, C.c_void_p, C.c_double
 
 class SgWindows(C.Structure):
     _fields_ = [("win_off", C.c_void_p), ("wins", C.c_void_p), ("nwin", C.c_void_p),
-                ("bm_off", C.c_void_p), ("bm_save", C.c_void_p)]
+                ("bm_off", C.c_void_p), ("bm_save", C.c_void_p), ("pre_save", C.c_void_p)]
 
 
 class SgTiers(C.Structure):

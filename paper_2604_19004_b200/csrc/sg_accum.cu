@@ -36,6 +36,9 @@
 namespace sg {
 
 constexpr int64_t NOLIMIT = 0x7fffffffffffffffll;
+#ifndef SG_UNR
+#define SG_UNR 4
+#endif
 
 struct Csr {
   const int64_t* ptr;
@@ -64,13 +67,96 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// One block of UNR x 32 products of a warp: per step, the lane's A value
+// multiplier (already applied) is carried as `a`, the gathered column and B
+// value are in registers; `valid` bit u marks steps with a product.
+template <int UNR>
+struct ProdBlock {
+  int32_t col[UNR];
+  double v[UNR];
+  unsigned valid;
+};
+
+// Resolve the owners of products [p0, p0 + 32*UNR) (advancing c0) and issue
+// their gathers.  Fast path (warp-uniform): the block lies inside one B-row
+// segment, so lanes read consecutive elements and no owner search is needed.
+template <bool VALUES, typename V, int UNR>
+__device__ __forceinline__ void plan_load(const Entries& E, int nent, int64_t p0, int64_t pend, int& c0,
+                                          const int32_t* __restrict__ b_col, const V* __restrict__ b_val,
+                                          unsigned le, ProdBlock<UNR>& B) {
+  const int lane = lane_id();
+  const int64_t blk_end = min(p0 + 32 * UNR, pend);
+  const int64_t seg_end = (c0 + 1 < nent) ? E.S[c0 + 1] : (int64_t)NOLIMIT;
+  B.valid = 0;
+  if (seg_end >= blk_end) {
+    const int64_t base = E.bs[c0] + (p0 - E.S[c0]) + lane;
+    const double a = VALUES ? E.av[c0] : 0.0;
+    const int nvalid = (int)(blk_end - p0) - lane;
+    const int32_t* cp = b_col + base;
+    const V* vp = b_val + base;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const bool ok = 32 * u < nvalid;
+#if defined(SG_PASS2_MODE) && SG_PASS2_MODE == 5
+      // experiment: operands from shared memory instead of L2 (wrong values)
+      extern __shared__ __align__(16) unsigned char smem[];
+      const int32_t* sc = reinterpret_cast<const int32_t*>(smem);
+      B.col[u] = ok ? sc[(lane + 32 * u) & 4095] + (int32_t)(base & 0) : 0;
+      B.v[u] = (VALUES && ok) ? a * 1.0 : 0.0;
+#else
+      B.col[u] = ok ? __ldg(cp + 32 * u) : 0;
+      B.v[u] = (VALUES && ok) ? a * (double)__ldg(vp + 32 * u) : 0.0;
+#endif
+      B.valid |= ok ? (1u << u) : 0u;
+    }
+    if (seg_end == blk_end) ++c0;
+    if (c0 >= nent) c0 = nent - 1;
+    return;
+  }
+  int64_t jj[UNR];
+  int cc[UNR];
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    const int64_t q0 = p0 + 32 * u;
+    const int ci = c0 + 1 + lane;
+    const int64_t nxt = ci < nent ? E.S[ci] : (int64_t)NOLIMIT;
+    const int64_t d = nxt - q0;
+    const unsigned bit = (d >= 0 && d < 32) ? (1u << (unsigned)d) : 0u;
+    const unsigned mask = __reduce_or_sync(SG_FULL, bit);
+    const int c = c0 + __popc(mask & le);
+    const int64_t p = q0 + lane;
+    cc[u] = c;
+    jj[u] = (p < pend) ? E.bs[c] + (p - E.S[c]) : -1;
+    const int k = __popc(mask);
+    const int64_t nk = __shfl_sync(SG_FULL, nxt, k);
+    c0 = c0 + k + (nk == q0 + 32 ? 1 : 0);
+    if (c0 >= nent) c0 = nent - 1;
+  }
+#pragma unroll
+  for (int u = 0; u < UNR; ++u) {
+    const bool ok = jj[u] >= 0;
+    B.col[u] = ok ? __ldg(b_col + jj[u]) : 0;
+    B.v[u] = (VALUES && ok) ? E.av[cc[u]] * (double)__ldg(b_val + jj[u]) : 0.0;
+    B.valid |= ok ? (1u << u) : 0u;
+  }
+}
+
+template <int UNR, class Op>
+__device__ __forceinline__ void run_ops(const ProdBlock<UNR>& B, Op& op) {
+#pragma unroll
+  for (int u = 0; u < UNR; ++u)
+    if (B.valid & (1u << u)) op(B.col[u], B.v[u]);
+}
+
 // The calling warp processes products [pbeg, pend) of a chunk; op(col, val).
+// Two-stage software pipeline: the gathers of block k+1 are in flight while
+// the (shared-memory) ops of block k run, so each lane keeps 2*UNR L2 round
+// trips outstanding instead of stalling on every block.
 template <bool VALUES, typename V, class Op>
 __device__ __forceinline__ void warp_products(const Entries& E, int nent, int64_t pbeg, int64_t pend,
                                               const int32_t* __restrict__ b_col,
                                               const V* __restrict__ b_val, Op& op) {
   if (pbeg >= pend) return;
-  const int lane = lane_id();
   int lo = 0, hi = nent - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
@@ -78,66 +164,35 @@ __device__ __forceinline__ void warp_products(const Entries& E, int nent, int64_
   }
   int c0 = lo;
   const unsigned le = lanemask_le();
-  // UNR steps of 32 products per iteration: owners are resolved first (shared
-  // memory + CREDUX only), then all UNR global loads are issued back to back
-  // so several L2/HBM round trips are in flight per lane.
-  constexpr int UNR = 4;
-  for (int64_t p0 = pbeg; p0 < pend; p0 += 32 * UNR) {
-    // fast path (warp-uniform): the whole 32*UNR block lies in one B-row
-    // segment, so lane products are consecutive elements of that row and no
-    // owner search is needed.  Long B rows (hubs) take this path.
-    const int64_t blk_end = min(p0 + 32 * UNR, pend);
-    const int64_t seg_end = (c0 + 1 < nent) ? E.S[c0 + 1] : (int64_t)NOLIMIT;
-    if (seg_end >= blk_end) {
-      const int64_t base = E.bs[c0] + (p0 - E.S[c0]) + lane;
-      const double a = VALUES ? E.av[c0] : 0.0;
-      const int nvalid = (int)(blk_end - p0) - lane;  // lanes with products in step u: 32u < nvalid
-      const int32_t* cp = b_col + base;
-      const V* vp = b_val + base;
-      int32_t col[UNR];
-      double bv[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const bool ok = 32 * u < nvalid;
-        col[u] = ok ? __ldg(cp + 32 * u) : 0;
-        bv[u] = (VALUES && ok) ? (double)__ldg(vp + 32 * u) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < UNR; ++u)
-        if (32 * u < nvalid) op(col[u], VALUES ? a * bv[u] : 0.0);
-      if (seg_end == blk_end) ++c0;
-      if (c0 >= nent) c0 = nent - 1;
-      continue;
+  constexpr int UNR = SG_UNR;
+  constexpr int STEP = 32 * UNR;
+  ProdBlock<UNR> A, Bk;
+  int64_t p = pbeg;
+  if (VALUES) {
+    // value passes are register-bound at 1024 threads: no prefetch stage
+    for (; p < pend; p += STEP) {
+      plan_load<VALUES, V, UNR>(E, nent, p, pend, c0, b_col, b_val, le, A);
+      run_ops(A, op);
     }
-    int64_t jj[UNR];
-    int cc[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int64_t q0 = p0 + 32 * u;
-      const int ci = c0 + 1 + lane;
-      const int64_t nxt = ci < nent ? E.S[ci] : (int64_t)NOLIMIT;
-      const int64_t d = nxt - q0;
-      const unsigned bit = (d >= 0 && d < 32) ? (1u << (unsigned)d) : 0u;
-      const unsigned mask = __reduce_or_sync(SG_FULL, bit);
-      const int c = c0 + __popc(mask & le);
-      const int64_t p = q0 + lane;
-      cc[u] = c;
-      jj[u] = (p < pend) ? E.bs[c] + (p - E.S[c]) : -1;
-      const int k = __popc(mask);
-      const int64_t nk = __shfl_sync(SG_FULL, nxt, k);
-      c0 = c0 + k + (nk == q0 + 32 ? 1 : 0);
-      if (c0 >= nent) c0 = nent - 1;
+    return;
+  }
+  plan_load<VALUES, V, UNR>(E, nent, p, pend, c0, b_col, b_val, le, A);
+  p += STEP;
+  for (;;) {
+    const bool hasB = p < pend;
+    if (hasB) {
+      plan_load<VALUES, V, UNR>(E, nent, p, pend, c0, b_col, b_val, le, Bk);
+      p += STEP;
     }
-    int32_t col[UNR];
-    double bv[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      col[u] = jj[u] >= 0 ? __ldg(b_col + jj[u]) : 0;
-      bv[u] = (VALUES && jj[u] >= 0) ? (double)__ldg(b_val + jj[u]) : 0.0;
+    run_ops(A, op);
+    if (!hasB) break;
+    const bool hasA = p < pend;
+    if (hasA) {
+      plan_load<VALUES, V, UNR>(E, nent, p, pend, c0, b_col, b_val, le, A);
+      p += STEP;
     }
-#pragma unroll
-    for (int u = 0; u < UNR; ++u)
-      if (jj[u] >= 0) op(col[u], VALUES ? E.av[cc[u]] * bv[u] : 0.0);
+    run_ops(Bk, op);
+    if (!hasA) break;
   }
 }
 
@@ -673,6 +728,7 @@ struct Win {
   int32_t* nwin;
   const int64_t* bm_off;
   unsigned long long* bm_save;
+  int32_t* pre_save;  // row-relative rank at the start of every saved word
 };
 
 // Symbolic-pass routing: rows counted with a shared-memory bitmap (and hence
@@ -770,9 +826,14 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
         int2* wrow = wins + win_off[row];
         const int64_t prev_last = last_id;
         if (win.bm_save) {
-          // keep the row's bitmap for the numeric windows (no second key pass)
+          // keep the row's bitmap and word ranks for the numeric windows and
+          // the column expansion (no second key pass, no second prefix)
           unsigned long long* dst = win.bm_save + win.bm_off[row] + gw0;
-          for (int i = threadIdx.x; i < nwords; i += NT) dst[i] = bm[i];
+          int32_t* pdst = win.pre_save + win.bm_off[row] + gw0;
+          for (int i = threadIdx.x; i < nwords; i += NT) {
+            dst[i] = bm[i];
+            pdst[i] = (int32_t)(total + pre[i]);
+          }
         }
         __syncthreads();
         const uint32_t tot32 = (uint32_t)total;
@@ -909,8 +970,17 @@ struct WinAddOp {
   __device__ __forceinline__ void operator()(int32_t col, double v) {
     const uint32_t x = (uint32_t)(col - c0);
     const uint32_t w = x >> 6;
+#if defined(SG_PASS2_MODE) && SG_PASS2_MODE == 4
+    // experiment: loads only (no rank, no accumulate)
+    if (v == 12345.678) vals[w & 15] = v;
+    return;
+#endif
     const int r = pre[w] + __popcll(bm[w] & ((2ull << (x & 63)) - 1ull)) - 1;
+#if defined(SG_PASS2_MODE) && SG_PASS2_MODE == 3
+    vals[r] += v;  // experiment: racy plain add (wrong values, timing only)
+#else
     smem_add(&vals[r], v);
+#endif
   }
 };
 
@@ -1017,6 +1087,7 @@ constexpr size_t bmr_smem() {
 template <typename V>
 __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinRun* __restrict__ work, Csr A, Csr B,
                                                    const unsigned long long* __restrict__ bm_save,
+                                                   const int32_t* __restrict__ pre_save,
                                                    int32_t* __restrict__ out_col, V* __restrict__ out_val,
                                                    unsigned long long* __restrict__ ticket) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1065,9 +1136,16 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinRun* 
       const int nwords = (int)(((int64_t)c1 - c0 + 63) >> 6);
       const bool saved = bm_save != nullptr;
       if (saved) {
-        // the count pass left this row's key bitmap: copy the window's words
-        const unsigned long long* src = bm_save + it->bm_base + ((c0 - it->lo) >> 6);
-        for (int i = threadIdx.x; i < nwords; i += WIN_NT) bm[i] = src[i];
+        // the count pass left this row's key bitmap and word ranks: copy the
+        // window's slice (columns are written by k_expand)
+        const int64_t wsrc = it->bm_base + ((c0 - it->lo) >> 6);
+        const unsigned long long* src = bm_save + wsrc;
+        const int32_t* psrc = pre_save + wsrc;
+        for (int i = threadIdx.x; i < nwords; i += WIN_NT) {
+          bm[i] = src[i];
+          pre[i] = psrc[i] - r0;
+        }
+        for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
       } else {
         for (int i = threadIdx.x; i < nwords; i += WIN_NT) bm[i] = 0ull;
       }
@@ -1115,17 +1193,19 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinRun* 
         }
       }
       SG_PH(2);
-      window_prefix(bm, pre, nwords, scr);
-      // columns first: expand the bitmap into a staging array that overlays
-      // the (not yet used) value slots, then copy it out coalesced
       const int64_t base = out_base + r0;
-      int* colbuf = reinterpret_cast<int*>(vals);
-      for (int i = threadIdx.x; i < nwords; i += WIN_NT) emit_bits_smem(bm[i], c0 + 64 * i, colbuf + pre[i]);
-      __syncthreads();
-      for (int i = threadIdx.x; i < cnt; i += WIN_NT) out_col[base + i] = colbuf[i];
-      __syncthreads();
-      for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
-      __syncthreads();
+      if (!saved) {
+        window_prefix(bm, pre, nwords, scr);
+        // columns first: expand the bitmap into a staging array that overlays
+        // the (not yet used) value slots, then copy it out coalesced
+        int* colbuf = reinterpret_cast<int*>(vals);
+        for (int i = threadIdx.x; i < nwords; i += WIN_NT) emit_bits_smem(bm[i], c0 + 64 * i, colbuf + pre[i]);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += WIN_NT) out_col[base + i] = colbuf[i];
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
+        __syncthreads();
+      }
       SG_PH(3);
       if (single) {
         block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
@@ -1150,6 +1230,30 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinRun* 
 #endif
     }
     b = item_next;
+  }
+}
+
+// Column expansion of the long rows from the saved key bitmaps and word
+// ranks: C.col_idx[row_ptr[row] + rank .. ] for every set bit, ascending.
+// One block per row (rows without windows are skipped), a word per thread,
+// per-lane bit loop straight to global memory.  (Staged/coalesced and
+// warp-cooperative variants measured slower on R-MAT-20.)
+constexpr int EXP_NT = 256;
+
+__global__ void __launch_bounds__(EXP_NT) k_expand(int64_t m, const int32_t* __restrict__ nwin,
+                                                   const int64_t* __restrict__ bm_off,
+                                                   const unsigned long long* __restrict__ bm_save,
+                                                   const int32_t* __restrict__ pre_save,
+                                                   const int64_t* __restrict__ span_lo,
+                                                   const int64_t* __restrict__ out_off,
+                                                   int32_t* __restrict__ out_col) {
+  for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
+    if (nwin[r] <= 0) continue;
+    const int64_t w0 = bm_off[r], nw = bm_off[r + 1] - w0;
+    const int32_t lo = (int32_t)span_lo[r];
+    int32_t* out = out_col + out_off[r];
+    for (int64_t i = threadIdx.x; i < nw; i += EXP_NT)
+      emit_bits(bm_save[w0 + i], lo + (int32_t)(64 * i), out + pre_save[w0 + i]);
   }
 }
 
@@ -1397,7 +1501,7 @@ static int launch_bm(const Launch& L, const int32_t* rows, int64_t n) {
   int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 32);
   kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.lo, L.hi, L.out_off, L.out_col,
                            (V*)L.out_val, L.counts, L.overflow,
-                           MODE == 0 ? L.win : Win{nullptr, nullptr, nullptr, nullptr, nullptr});
+                           MODE == 0 ? L.win : Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
   return check_cuda("k_bitmap");
 }
 
@@ -1466,9 +1570,10 @@ using namespace sg;
 extern "C" {
 
 static Win to_win(const sg_windows_t* w) {
-  if (!w) return Win{nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (!w) return Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  const bool sv = w->bm_save != nullptr && w->pre_save != nullptr;
   return Win{w->win_off, reinterpret_cast<int2*>(w->wins), w->nwin, w->bm_off,
-             reinterpret_cast<unsigned long long*>(w->bm_save)};
+             sv ? reinterpret_cast<unsigned long long*>(w->bm_save) : nullptr, sv ? w->pre_save : nullptr};
 }
 
 int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col, const int64_t* b_ptr,
@@ -1596,14 +1701,19 @@ int sg_window_numeric(int64_t m, int dtype, const int64_t* a_ptr, const int32_t*
   constexpr size_t sm = bmr_smem();
   const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
   const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms());
+  if (W.bm_save) {
+    k_expand<<<(int)std::min<int64_t>(m, (int64_t)num_sms() * 16), EXP_NT, 0, s>>>(
+        m, W.nwin, W.bm_off, W.bm_save, W.pre_save, span_lo, out_off, out_col);
+    if (int rc = check_cuda("k_expand")) return rc;
+  }
   if (dtype == SG_F64) {
     auto kern = k_bmr<double>;
     if (int rc = set_smem(kern, sm)) return rc;
-    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, W.bm_save, out_col, (double*)out_val, ticket);
+    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, W.bm_save, W.pre_save, out_col, (double*)out_val, ticket);
   } else {
     auto kern = k_bmr<float>;
     if (int rc = set_smem(kern, sm)) return rc;
-    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, W.bm_save, out_col, (float*)out_val, ticket);
+    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, W.bm_save, W.pre_save, out_col, (float*)out_val, ticket);
   }
   return check_cuda("k_bmr");
 }

@@ -144,8 +144,9 @@ def scan(ctx: _Ctx, x):
 class Windows:
     """Numeric window tables of the long rows (sg_windows_t, include/sgb200.h)."""
 
-    def __init__(self, off, wins, nwin, bm_off, bm_save, total):
-        self.off, self.wins, self.nwin, self.bm_off, self.bm_save, self.total = off, wins, nwin, bm_off, bm_save, total
+    def __init__(self, off, wins, nwin, bm_off, bm_save, pre_save, total):
+        self.off, self.wins, self.nwin, self.bm_off, self.total = off, wins, nwin, bm_off, total
+        self.bm_save, self.pre_save = bm_save, pre_save
         self._struct = None
 
     def struct(self):
@@ -153,12 +154,14 @@ class Windows:
         s.win_off, s.wins, s.nwin = ptr(self.off), ptr(self.wins), ptr(self.nwin)
         s.bm_off = ptr(self.bm_off) if self.bm_save is not None else None
         s.bm_save = ptr(self.bm_save) if self.bm_save is not None else None
+        s.pre_save = ptr(self.pre_save) if self.bm_save is not None else None
         self._struct = s  # keep alive for the call
         return s
 
     def drop_bitmaps(self):
         """Release the saved key bitmaps (the window pass then rebuilds keys)."""
         self.bm_save = None
+        self.pre_save = None
 
 
 # saved key bitmaps may use at most this share of the free device memory
@@ -175,17 +178,18 @@ def windows(ctx: _Ctx, m, products, lo, hi, select) -> Windows:
     total, words = int(totals[0]), int(totals[1])
     wins = torch.full((max(2 * total, 2),), -1, dtype=torch.int32, device=ctx.device)
     nwin = torch.zeros(max(m, 1), dtype=torch.int32, device=ctx.device)
-    bm_save = None
+    bm_save = pre_save = None
     if total and words:
         free, _ = torch.cuda.mem_get_info(ctx.device)
         # blocks cached by torch's allocator are free for this purpose too
         free += torch.cuda.memory_reserved(ctx.device) - torch.cuda.memory_allocated(ctx.device)
-        if 8 * words <= BITMAP_SAVE_SHARE * free:
+        if 12 * words <= BITMAP_SAVE_SHARE * free:
             try:
                 bm_save = torch.empty(words, dtype=torch.int64, device=ctx.device)
+                pre_save = torch.empty(words, dtype=torch.int32, device=ctx.device)
             except torch.OutOfMemoryError:
-                bm_save = None
-    return Windows(off, wins, nwin, bm_off, bm_save, total)
+                bm_save = pre_save = None
+    return Windows(off, wins, nwin, bm_off, bm_save, pre_save, total)
 
 
 def alloc_c(ctx: _Ctx, nnz, dtype, win):

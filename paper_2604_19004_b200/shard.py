@@ -185,6 +185,22 @@ def gather_shards(shard: Shard, counts, cuts, root, group, device):
     return Shard(0, nrows, 0, total, row_ptr, col, val, shard.report)
 
 
+def gpu_products_fn(device):
+    """products_fn for the root on a GPU: the row-stats kernel (analysis.py:96-128)."""
+    from .device import DeviceCsr
+    from .engine import _Ctx, row_stats
+
+    def fn(a_ptr, a_col, b_ptr):
+        ctx = _Ctx(device, torch.cuda.current_stream(device))
+        m = a_ptr.numel() - 1
+        A = DeviceCsr(m, b_ptr.numel() - 1, a_ptr, a_col, torch.empty(0, device=device))
+        B = DeviceCsr(b_ptr.numel() - 1, 0, b_ptr, torch.empty(0, dtype=torch.int32, device=device),
+                      torch.empty(0, device=device))
+        prod, _, _, _ = row_stats(ctx, A, B)
+        return prod.cpu().numpy()
+    return fn
+
+
 def gpu_local_fn(cfg):
     """local_fn running the single-GPU engine on this rank's device."""
     from .device import DeviceCsr
@@ -197,5 +213,6 @@ def gpu_local_fn(cfg):
         Ad = DeviceCsr(nrows, ncols_a, row_ptr, col_idx, values)
         Bd = DeviceCsr(B[0], B[1], B[2], B[3], B[4])
         c, rep = spgemm(Ad, Bd, cfg)
+        rep.nrows_local = nrows
         return c.row_ptr, c.col_idx, c.values, rep
     return fn
