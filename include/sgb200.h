@@ -102,8 +102,9 @@ int sg_hll_estimate(int64_t nsel, const int64_t* rows, const int64_t* a_ptr,
  *  pre_save int32[bm_off[m]] row-relative rank at each saved word (with
  *           bm_save; lets the numeric pass skip the prefix and write C's
  *           columns with a separate streaming expansion)
- * Each window holds at most 16384 distinct columns over at most 262144
- * columns, so its bitmap, rank prefix and values sit in shared memory. */
+ * Windows start on 4096-column tiles and hold at most 16384 distinct columns
+ * over at most 262144 columns, so a window's bitmap, rank prefix and values
+ * sit in shared memory. */
 typedef struct sg_windows {
   const int64_t* win_off;
   int32_t* wins;
@@ -111,7 +112,21 @@ typedef struct sg_windows {
   const int64_t* bm_off;
   uint64_t* bm_save;
   int32_t* pre_save;
+  const int64_t* btile_off; /* B tile index (sg_btile_plan/build), or NULL */
+  const int32_t* btile;
 } sg_windows_t;
+
+/* B tile index: for the longest B rows (as many as fit budget_bytes), the
+ * offset within the row of the first column >= t*4096 for every tile t, so
+ * the numeric windows (which start on 4096-column tiles) clip B rows with two
+ * lookups instead of binary searches.  sg_btile_plan writes tbl_scan
+ * int64[k+1] (exclusive scan of table sizes), totals_host[0] = table entries,
+ * totals_host[1] = minimum indexed row length (-1: none); sg_btile_build then
+ * fills tbl_off int64[k] (-1 for rows without a table) and tbl int32[]. */
+int sg_btile_plan(int64_t k, int64_t b_ncols, const int64_t* b_ptr, int64_t budget_bytes,
+                  int64_t* tbl_scan, int64_t* totals_host, void* ws, size_t ws_bytes, void* stream);
+int sg_btile_build(int64_t k, int64_t b_ncols, const int64_t* b_ptr, const int32_t* b_col,
+                   const int64_t* tbl_scan, int64_t* tbl_off, int32_t* tbl, void* stream);
 
 /* Sizes the window tables for rows with select[row] != 0 (all rows when
  * select == NULL): writes win_off and, if bm_off != NULL, bm_off (both
@@ -131,16 +146,18 @@ int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t*
                 const int64_t* span_lo, const int64_t* span_hi, int64_t* counts,
                 const sg_windows_t* win, void* ws, size_t ws_bytes, void* stream);
 
-/* Long-row numeric pass over the recorded windows: one CTA per run of <= 8
- * windows of a row, values accumulated in shared memory (fp64), columns and
- * values written sorted at out_off[row] + rank (out_off = row_ptr of C).
- * work_buf: 120 bytes x work_cap scratch, work_cap >= total windows. */
-int sg_window_numeric(int64_t m, int dtype, const int64_t* a_ptr, const int32_t* a_col,
-                      const void* a_val, const int64_t* b_ptr, const int32_t* b_col,
-                      const void* b_val, const int64_t* span_lo, const int64_t* span_hi,
-                      const sg_windows_t* win, const int64_t* out_off, int32_t* out_col,
-                      void* out_val, void* work_buf, int64_t work_cap, void* ws, size_t ws_bytes,
-                      void* stream);
+/* Long-row numeric pass over the recorded windows: one CTA (1024 threads)
+ * per window, work grouped by column range so concurrent CTAs share B-row
+ * slabs in L2; values accumulated in shared memory (fp64) and written sorted
+ * at out_off[row] + rank (out_off = row_ptr of C).  With saved bitmaps the
+ * columns are written by a separate streaming expansion.  work_buf: 48 bytes
+ * x work_cap scratch, work_cap >= total windows. */
+int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr,
+                      const int32_t* a_col, const void* a_val, const int64_t* b_ptr,
+                      const int32_t* b_col, const void* b_val, const int64_t* span_lo,
+                      const int64_t* span_hi, const sg_windows_t* win, const int64_t* out_off,
+                      int32_t* out_col, void* out_val, void* work_buf, int64_t work_cap, void* ws,
+                      size_t ws_bytes, void* stream);
 
 /* Replaces accumulate.plan_rows (accumulate.py:104-181) with the identical
  * integer rules.  pred is int64 (EXACT / UPPER) or f64 (ESTIMATED). */

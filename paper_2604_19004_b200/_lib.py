@@ -23,7 +23,8 @@ I64, I32, SZ, P, D = C.c_int64, C.c_int, C.c_size_t, C.c_void_p, C.c_double
 
 class SgWindows(C.Structure):
     _fields_ = [("win_off", C.c_void_p), ("wins", C.c_void_p), ("nwin", C.c_void_p),
-                ("bm_off", C.c_void_p), ("bm_save", C.c_void_p), ("pre_save", C.c_void_p)]
+                ("bm_off", C.c_void_p), ("bm_save", C.c_void_p), ("pre_save", C.c_void_p),
+                ("btile_off", C.c_void_p), ("btile", C.c_void_p)]
 
 
 class SgTiers(C.Structure):
@@ -43,8 +44,10 @@ SIGNATURES = {
     "sg_hll_estimate": (I32, [I64, P, P, P, P, I32, P, D, P, P]),
     "sg_window_capacity": (I32, [I64, P, P, P, P, P, P, P, P, SZ, P]),
     "sg_symbolic": (I32, [I64, I64, P, P, P, P, P, P, P, P, C.POINTER(SgWindows), P, SZ, P]),
-    "sg_window_numeric": (I32, [I64, I32, P, P, P, P, P, P, P, P, C.POINTER(SgWindows), P, P, P, P, I64,
-                                P, SZ, P]),
+    "sg_window_numeric": (I32, [I64, I64, I32, P, P, P, P, P, P, P, P, C.POINTER(SgWindows), P, P, P, P,
+                                I64, P, SZ, P]),
+    "sg_btile_plan": (I32, [I64, I64, P, I64, P, P, P, SZ, P]),
+    "sg_btile_build": (I32, [I64, I64, P, P, P, P, P, P]),
     "sg_plan": (I32, [I64, I32, P, P, P, P, C.POINTER(SgTiers), P, P, P, P]),
     "sg_scan": (I32, [I64, P, P, P, SZ, P]),
     "sg_numeric": (I32, [I64, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),

@@ -435,8 +435,8 @@ __global__ void __launch_bounds__(HW_WARPS * 32) k_hash_warp(int64_t nbin, const
   bitonic_kv(keys, vals, pad, lane, 32, WarpSync{});
   const int64_t off = out_off[row];
   for (int i = lane; i < n; i += 32) {
-    out_col[off + i] = keys[i];
-    out_val[off + i] = (V)vals[i];
+    st_stream(out_col + off + i, keys[i]);
+    st_stream(out_val + off + i, (V)vals[i]);
   }
   if (lane == 0) {
     counts[row] = n;
@@ -537,8 +537,8 @@ __global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* 
       for (int i = 0; i < ITEMS; ++i) {
         const int idx = i * NT + threadIdx.x;
         if (idx < n) {
-          out_col[off + idx] = (int32_t)kk[i] + lo32;
-          out_val[off + idx] = (V)vv[i];
+          st_stream(out_col + off + idx, (int32_t)kk[i] + lo32);
+          st_stream(out_val + off + idx, (V)vv[i]);
         }
       }
     }
@@ -629,8 +629,8 @@ __global__ void __launch_bounds__(ESC_WARPS * 32) k_esc(int64_t nbin, const int3
       double s = vsorted[w][i];
       for (int r = i + 1; r < np && (key[w][r] >> 32) == (key[w][i] >> 32); ++r) s += vsorted[w][r];
       const int pos = nhead + __popc(hb & lanemask_lt());
-      out_col[off + pos] = (int32_t)(key[w][i] >> 32);
-      out_val[off + pos] = (V)s;
+      st_stream(out_col + off + pos, (int32_t)(key[w][i] >> 32));
+      st_stream(out_val + off + pos, (V)s);
     }
     nhead += __popc(hb);
   }
@@ -703,11 +703,11 @@ __device__ __forceinline__ void emit_bits(unsigned long long bits, int32_t colba
   unsigned lo = (unsigned)bits, hi = (unsigned)(bits >> 32);
   int k = 0;
   while (lo) {
-    out[k++] = colbase + __ffs(lo) - 1;
+    st_stream(out + k++, colbase + __ffs(lo) - 1);
     lo &= lo - 1;
   }
   while (hi) {
-    out[k++] = colbase + 31 + __ffs(hi);
+    st_stream(out + k++, colbase + 31 + __ffs(hi));
     hi &= hi - 1;
   }
 }
@@ -718,8 +718,16 @@ __device__ __forceinline__ void emit_bits(unsigned long long bits, int32_t colba
 // all sit in shared memory.
 constexpr int WIN_WORDS = 4096;  // 262,144 columns
 constexpr int WIN_R = 16384;     // values per window (128 KB fp64)
-constexpr int WIN_RP = WIN_R - 64;
+// Windows start on TILE_COLS-column tiles (absolute), so each selected B
+// row's segment in a window is two lookups in the B tile index (no search).
+constexpr int TILE_COLS = 4096;
+constexpr int TILE_WORDS = TILE_COLS / 64;
+constexpr int WIN_RP = WIN_R - TILE_COLS;  // a tile adds at most TILE_COLS keys
+constexpr int WIN_TILES = WIN_WORDS / TILE_WORDS;
 constexpr int WIN_NT = 1024;
+
+// bitmap origin of a windowed row: span_lo rounded down to a tile
+__host__ __device__ __forceinline__ int64_t win_origin(int64_t lo) { return lo & ~(int64_t)(TILE_COLS - 1); }
 
 // device view of sg_windows_t (include/sgb200.h)
 struct Win {
@@ -729,6 +737,8 @@ struct Win {
   const int64_t* bm_off;
   unsigned long long* bm_save;
   int32_t* pre_save;  // row-relative rank at the start of every saved word
+  const int64_t* btile_off;
+  const int32_t* btile;
 };
 
 // Symbolic-pass routing: rows counted with a shared-memory bitmap (and hence
@@ -743,7 +753,7 @@ __host__ __device__ __forceinline__ bool count_uses_bitmap(int64_t p, int64_t sp
 __host__ __device__ __forceinline__ int64_t window_capacity(int64_t products, int64_t span) {
   if (products <= 0 || span <= 0) return 0;
   const int64_t d = products < span ? products : span;
-  return d / WIN_RP + ((span - 1) / 64) / WIN_WORDS + 1;
+  return d / WIN_RP + (span + TILE_COLS) / TILE_COLS / WIN_TILES + 2;
 }
 
 template <int BW, int MODE, typename V, int NT>
@@ -803,7 +813,9 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
       __syncthreads();
       continue;
     }
-    for (int64_t wlo = lo; wlo <= hi; wlo += WCOLS) {
+    // windowed rows (count pass) keep their bitmap from a tile-aligned origin
+    const int64_t org = (MODE == 0 && wcap > 0) ? win_origin(lo) : lo;
+    for (int64_t wlo = org; wlo <= hi; wlo += WCOLS) {
       const int64_t whi = min(hi, wlo + WCOLS - 1);
       const int nwords = (int)((whi - wlo) / 64 + 1);
       for (int i = threadIdx.x; i < nwords; i += NT) bm[i] = 0ull;
@@ -820,9 +832,11 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
       }
       const int64_t wtot = bitmap_prefix<NT>(bm, pre, nwords, scr);
       if (MODE == 0) {
-        // emit numeric windows: word gw (relative to lo) starts window
-        // id = rank/WIN_RP + gw/WIN_WORDS whenever the id changes
-        const int64_t gw0 = (wlo - lo) >> 6;
+        // emit numeric windows.  Tile t (TILE_WORDS words, relative to the
+        // tile-aligned origin) belongs to window id = rank(t)/WIN_RP +
+        // t/WIN_TILES with rank(t) the row rank of the tile's first column;
+        // a window starts at every tile whose id differs from the previous.
+        const int64_t gw0 = (wlo - org) >> 6;  // count windows are tile-aligned
         int2* wrow = wins + win_off[row];
         const int64_t prev_last = last_id;
         if (win.bm_save) {
@@ -831,24 +845,26 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
           unsigned long long* dst = win.bm_save + win.bm_off[row] + gw0;
           int32_t* pdst = win.pre_save + win.bm_off[row] + gw0;
           for (int i = threadIdx.x; i < nwords; i += NT) {
-            dst[i] = bm[i];
-            pdst[i] = (int32_t)(total + pre[i]);
+            st_stream(dst + i, bm[i]);
+            st_stream(pdst + i, (int32_t)(total + pre[i]));
           }
         }
         __syncthreads();
         const uint32_t tot32 = (uint32_t)total;
-        for (int i = threadIdx.x; i < nwords; i += NT) {
-          const uint32_t gw = (uint32_t)gw0 + (uint32_t)i;
-          const uint32_t rank = tot32 + (uint32_t)pre[i];
-          const int64_t id = (int64_t)(rank / (uint32_t)WIN_RP + gw / (uint32_t)WIN_WORDS);
+        const int ntiles = (nwords + TILE_WORDS - 1) / TILE_WORDS;
+        for (int ti = threadIdx.x; ti < ntiles; ti += NT) {
+          const uint32_t t = (uint32_t)(gw0 / TILE_WORDS) + (uint32_t)ti;
+          const uint32_t rank = tot32 + (uint32_t)pre[ti * TILE_WORDS];
+          const int64_t id = (int64_t)(rank / (uint32_t)WIN_RP + t / (uint32_t)WIN_TILES);
           int64_t idp = -1;
-          if (i > 0) {
-            idp = (int64_t)((tot32 + (uint32_t)pre[i - 1]) / (uint32_t)WIN_RP + (gw - 1) / (uint32_t)WIN_WORDS);
-          } else if (gw > 0) {
+          if (ti > 0) {
+            idp = (int64_t)((tot32 + (uint32_t)pre[(ti - 1) * TILE_WORDS]) / (uint32_t)WIN_RP +
+                            (t - 1) / (uint32_t)WIN_TILES);
+          } else if (t > 0) {
             idp = prev_last;
           }
-          if (id != idp && id < wcap) wrow[id] = make_int2((int)(lo + 64 * (int64_t)gw), (int)rank);
-          if (i == nwords - 1) last_id = id;
+          if (id != idp && id < wcap) wrow[id] = make_int2((int)(org + (int64_t)TILE_COLS * t), (int)rank);
+          if (ti == ntiles - 1) last_id = id;
         }
         total += wtot;
         __syncthreads();
@@ -1060,33 +1076,78 @@ __device__ __forceinline__ int nth_set_bit64(unsigned long long x, int k) {
   return pos + (k >= (int)(v & 1u) ? 1 : 0);
 }
 
-// A run of up to WRUN consecutive windows of one row.  Window i covers
-// columns [cb[i], cb[i+1]) and ranks [rk[i], rk[i+1]) of the row.
-constexpr int WRUN = 8;
-struct WinRun {
-  int64_t out_base;  // C index of the row's first entry
+// One numeric window, resolved before launch: a CTA needs a single load.
+struct WinItem {
+  int64_t out_base;  // C index of the window's first entry (row_ptr + rank)
   int64_t t0;        // A row start
+  int64_t bm_word;   // saved-bitmap word of the window's first column (-1: none)
   int32_t t_len;     // A row length
-  int32_t nw;        // windows in this run
-  int32_t first;     // cb[0] is the row's first column (no lower-bound search)
-  int32_t last;      // cb[nw] is past the row's last column (no upper search)
-  int64_t bm_base;   // word offset of the row's saved bitmap (if any)
-  int32_t lo;        // the row's first output column (bitmap word 0)
+  int32_t c0, c1;    // columns [c0, c1); c0 tile-aligned, c1 tile-aligned or row end
+  int32_t cnt;       // distinct columns in the window
+  int32_t last;      // window ends at the row's end (segment = rest of B row)
   int32_t pad;
-  int32_t cb[WRUN + 1];
-  int32_t rk[WRUN + 1];
 };
 
-constexpr size_t bmr_smem() {
-  return (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8 + (size_t)3 * (WIN_NT + 1) * 8 + (size_t)WIN_NT * 16;
+// B tile index: for B rows with a table, tbl[tbl_off[k] + t] = offset in the
+// row of the first column >= t*TILE_COLS (t = 0..ceil(ncols/TILE_COLS)).
+struct BTile {
+  const int64_t* off;  // int64[k]: table start, or -1
+  const int32_t* tbl;
+};
+
+// Clip the B rows of a chunk of A entries to columns [c0, c1) (table lookup
+// when indexed, binary search otherwise) and compact the non-empty segments.
+template <bool VALUES, typename V>
+__device__ __forceinline__ int64_t block_load_tiles(int64_t t, int64_t t1, int32_t c0, int32_t c1, bool last,
+                                                    const int32_t* __restrict__ a_col, const V* __restrict__ a_val,
+                                                    const int64_t* __restrict__ b_ptr,
+                                                    const int32_t* __restrict__ b_col, BTile bt, Entries E,
+                                                    int64_t* scr, int& nent) {
+  int64_t bs = 0, len = 0;
+  double av = 0.0;
+  if (t + threadIdx.x < t1) {
+    const int32_t k = a_col[t + threadIdx.x];
+    const int64_t s = b_ptr[k], e = b_ptr[k + 1];
+    if (e > s) {
+      const int64_t to = bt.off ? bt.off[k] : -1;
+      int64_t ss, ee;
+      if (to >= 0) {
+        ss = s + bt.tbl[to + c0 / TILE_COLS];
+        ee = (last || (c1 % TILE_COLS)) ? e : s + bt.tbl[to + c1 / TILE_COLS];
+        if (last) ee = e;
+      } else {
+        ss = lower_bound_col(b_col, s, e, c0);
+        ee = last ? e : lower_bound_col(b_col, ss, e, c1);
+      }
+      bs = ss;
+      len = ee - ss;
+    }
+    if (VALUES) av = (double)a_val[t + threadIdx.x];
+  }
+  int64_t P, n64;
+  const int64_t S = block_excl_scan(len, scr, &P);
+  const int64_t pos = block_excl_scan((int64_t)(len > 0), scr, &n64);
+  if (len > 0) {
+    E.S[pos] = S;
+    E.bs[pos] = bs;
+    if (VALUES) E.av[pos] = av;
+  }
+  __syncthreads();
+  nent = (int)n64;
+  return P;
 }
 
-// One CTA per run.  Rows whose A row fits one chunk keep a per-entry cursor
-// in shared memory, so window w+1 starts where window w stopped and each
-// window needs at most one lower_bound per entry (none for the last window).
+constexpr size_t bmr_smem() {
+  return (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8 + (size_t)3 * (WIN_NT + 1) * 8;
+}
+
+// One CTA per window (dynamic tickets; items are grouped by column range so
+// concurrent CTAs gather the same B-row slabs and keep them in L2).  With the
+// saved key bitmap and word ranks the window needs one value pass: rank =
+// pre[w] + popc(bits below), fp64 add into shared memory, coalesced write.
 template <typename V>
-__global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinRun* __restrict__ work, Csr A, Csr B,
-                                                   const unsigned long long* __restrict__ bm_save,
+__global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinItem* __restrict__ work, Csr A, Csr B,
+                                                   BTile bt, const unsigned long long* __restrict__ bm_save,
                                                    const int32_t* __restrict__ pre_save,
                                                    int32_t* __restrict__ out_col, V* __restrict__ out_val,
                                                    unsigned long long* __restrict__ ticket) {
@@ -1099,8 +1160,6 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinRun* 
   unsigned char* ebase = smem + (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8;
   Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (WIN_NT + 1),
             reinterpret_cast<double*>(ebase) + 2 * (WIN_NT + 1)};
-  int64_t* cur = reinterpret_cast<int64_t*>(ebase + (size_t)3 * (WIN_NT + 1) * 8);
-  int64_t* end = cur + WIN_NT;
   const V* av = (const V*)A.val;
   const V* bv = (const V*)B.val;
   if (threadIdx.x == 0) item_next = (int64_t)atomicAdd(ticket, 1ull);
@@ -1110,125 +1169,84 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinRun* 
   long long _tprev = clock64();
 #endif
   while (b < nwork) {
-    const WinRun* it = work + b;
-    const int64_t t0 = it->t0;
-    const int tl = it->t_len;
-    const int nw = it->nw;
-    const int first = it->first, last = it->last;
-    const int64_t out_base = it->out_base;
+    const WinItem it = work[b];
     __syncthreads();  // everyone has read item_next
     if (threadIdx.x == 0) item_next = (int64_t)atomicAdd(ticket, 1ull);
-    const bool single = tl <= WIN_NT;
-    double my_av = 0.0;
-    if (single && (int)threadIdx.x < tl) {
-      const int32_t k = A.col[t0 + threadIdx.x];
-      int64_t s = B.ptr[k];
-      const int64_t e = B.ptr[k + 1];
-      if (!first && s < e && __ldg(B.col + s) < it->cb[0]) s = lower_bound_col(B.col, s, e, it->cb[0]);
-      cur[threadIdx.x] = s;
-      end[threadIdx.x] = e;
-      my_av = (double)av[t0 + threadIdx.x];
+    const int32_t c0 = it.c0, c1 = it.c1;
+    const int cnt = it.cnt;
+    const int nwords = (int)(((int64_t)c1 - c0 + 63) >> 6);
+    const bool saved = it.bm_word >= 0 && bm_save != nullptr;
+    if (saved) {
+      const unsigned long long* src = bm_save + it.bm_word;
+      const int32_t* psrc = pre_save + it.bm_word;
+      const int r0 = __ldcs(psrc);
+      for (int i = threadIdx.x; i < nwords; i += WIN_NT) {
+        bm[i] = __ldcs(src + i);
+        pre[i] = __ldcs(psrc + i) - r0;
+      }
+    } else {
+      for (int i = threadIdx.x; i < nwords; i += WIN_NT) bm[i] = 0ull;
     }
-    for (int w = 0; w < nw; ++w) {
-      const int32_t c0 = it->cb[w], c1 = it->cb[w + 1];
-      const int r0 = it->rk[w];
-      const int cnt = it->rk[w + 1] - r0;
-      const int nwords = (int)(((int64_t)c1 - c0 + 63) >> 6);
-      const bool saved = bm_save != nullptr;
-      if (saved) {
-        // the count pass left this row's key bitmap and word ranks: copy the
-        // window's slice (columns are written by k_expand)
-        const int64_t wsrc = it->bm_base + ((c0 - it->lo) >> 6);
-        const unsigned long long* src = bm_save + wsrc;
-        const int32_t* psrc = pre_save + wsrc;
-        for (int i = threadIdx.x; i < nwords; i += WIN_NT) {
-          bm[i] = src[i];
-          pre[i] = psrc[i] - r0;
-        }
-        for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
-      } else {
-        for (int i = threadIdx.x; i < nwords; i += WIN_NT) bm[i] = 0ull;
-      }
-      __syncthreads();
-      SG_PH(0);
-      WinSetOp so{reinterpret_cast<unsigned*>(bm), c0};
-      WinAddOp ao{bm, pre, vals, c0};
-      int nent = 0;
-      int64_t P = 0;
-      if (single) {
-        int64_t s = 0, len = 0;
-        if ((int)threadIdx.x < tl) {
-          s = cur[threadIdx.x];
-          const int64_t e = end[threadIdx.x];
-          int64_t ee = e;
-          if (!(last && w == nw - 1) && s < e) {
-            if (__ldg(B.col + e - 1) >= c1) ee = (__ldg(B.col + s) >= c1) ? s : lower_bound_col(B.col, s, e, c1);
-          }
-          len = ee - s;
-          cur[threadIdx.x] = ee;
-        }
-        const int64_t S = block_excl_scan(len, scr, &P);
-        int64_t n64;
-        const int64_t pos = block_excl_scan((int64_t)(len > 0), scr, &n64);
-        if (len > 0) {
-          E.S[pos] = S;
-          E.bs[pos] = s;
-          E.av[pos] = my_av;
-        }
-        __syncthreads();
-        nent = (int)n64;
-        SG_PH(1);
+    for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
+    __syncthreads();
+    SG_PH(0);
+    WinSetOp so{reinterpret_cast<unsigned*>(bm), c0};
+    WinAddOp ao{bm, pre, vals, c0};
+    const int64_t t0 = it.t0, t1 = it.t0 + it.t_len;
+    const bool single = it.t_len <= WIN_NT;
+    int nent = 0;
+    int64_t P = 0;
+    if (single) {
+      P = block_load_tiles<true, V>(t0, t1, c0, c1, it.last, A.col, av, B.ptr, B.col, bt, E, scr, nent);
+      SG_PH(1);
 #ifdef SG_PROF
-        if (threadIdx.x == 0) atomicAdd(&g_phase[8], (unsigned long long)P);
+      if (threadIdx.x == 0) atomicAdd(&g_phase[8], (unsigned long long)P);
 #endif
-        if (!saved) {
-          block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
-          __syncthreads();
-        }
-      } else if (!saved) {
-        for (int64_t t = t0; t < t0 + tl; t += WIN_NT) {
-          P = block_load_range<false, V>(t, t0 + tl, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
-          block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
-          __syncthreads();
-        }
-      }
-      SG_PH(2);
-      const int64_t base = out_base + r0;
-      if (!saved) {
-        window_prefix(bm, pre, nwords, scr);
-        // columns first: expand the bitmap into a staging array that overlays
-        // the (not yet used) value slots, then copy it out coalesced
-        int* colbuf = reinterpret_cast<int*>(vals);
-        for (int i = threadIdx.x; i < nwords; i += WIN_NT) emit_bits_smem(bm[i], c0 + 64 * i, colbuf + pre[i]);
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += WIN_NT) out_col[base + i] = colbuf[i];
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
-        __syncthreads();
-      }
-      SG_PH(3);
+    }
+    if (!saved) {
+      // no saved keys: key pass, rank prefix, column emission (staging
+      // buffer overlays the value slots, then zero them again)
       if (single) {
+        block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
+        __syncthreads();
+      } else {
+        for (int64_t t = t0; t < t1; t += WIN_NT) {
+          P = block_load_tiles<false, V>(t, t1, c0, c1, it.last, A.col, av, B.ptr, B.col, bt, E, scr, nent);
+          block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
+          __syncthreads();
+        }
+      }
+      window_prefix(bm, pre, nwords, scr);
+      int* colbuf = reinterpret_cast<int*>(vals);
+      for (int i = threadIdx.x; i < nwords; i += WIN_NT) emit_bits_smem(bm[i], c0 + 64 * i, colbuf + pre[i]);
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt; i += WIN_NT) st_stream(out_col + it.out_base + i, colbuf[i]);
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
+      __syncthreads();
+    }
+    SG_PH(2);
+    if (single) {
+      block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
+      __syncthreads();
+    } else {
+      for (int64_t t = t0; t < t1; t += WIN_NT) {
+        P = block_load_tiles<true, V>(t, t1, c0, c1, it.last, A.col, av, B.ptr, B.col, bt, E, scr, nent);
         block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
         __syncthreads();
-      } else {
-        for (int64_t t = t0; t < t0 + tl; t += WIN_NT) {
-          P = block_load_range<true, V>(t, t0 + tl, c0, c1, A.col, av, B.ptr, B.col, E, scr, nent);
-          block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
-          __syncthreads();
-        }
       }
-      SG_PH(4);
-      for (int i = threadIdx.x; i < cnt; i += WIN_NT) out_val[base + i] = (V)vals[i];
-      __syncthreads();
-      SG_PH(5);
-#ifdef SG_PROF
-      if (threadIdx.x == 0) {
-        atomicAdd(&g_phase[9], 1ull);
-        atomicAdd(&g_phase[10], (unsigned long long)nwords);
-        atomicAdd(&g_phase[11], (unsigned long long)cnt);
-      }
-#endif
     }
+    SG_PH(4);
+    for (int i = threadIdx.x; i < cnt; i += WIN_NT) st_stream(out_val + it.out_base + i, (V)vals[i]);
+    __syncthreads();
+    SG_PH(5);
+#ifdef SG_PROF
+    if (threadIdx.x == 0) {
+      atomicAdd(&g_phase[9], 1ull);
+      atomicAdd(&g_phase[10], (unsigned long long)nwords);
+      atomicAdd(&g_phase[11], (unsigned long long)cnt);
+    }
+#endif
     b = item_next;
   }
 }
@@ -1250,71 +1268,113 @@ __global__ void __launch_bounds__(EXP_NT) k_expand(int64_t m, const int32_t* __r
   for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
     if (nwin[r] <= 0) continue;
     const int64_t w0 = bm_off[r], nw = bm_off[r + 1] - w0;
-    const int32_t lo = (int32_t)span_lo[r];
+    const int32_t org = (int32_t)win_origin(span_lo[r]);
     int32_t* out = out_col + out_off[r];
     for (int64_t i = threadIdx.x; i < nw; i += EXP_NT)
-      emit_bits(bm_save[w0 + i], lo + (int32_t)(64 * i), out + pre_save[w0 + i]);
+      emit_bits(__ldcs(bm_save + w0 + i), org + (int32_t)(64 * i), out + __ldcs(pre_save + w0 + i));
   }
 }
 
-// runs per row (used windows / WRUN, rounded up)
-__global__ void k_win_counts(int64_t m, const int64_t* __restrict__ win_off, const int2* __restrict__ wins,
-                             const int32_t* __restrict__ nwin, int64_t* __restrict__ n_out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const int n = nwin[i];
-  int c = 0;
-  if (n > 0) {
-    const int2* wr = wins + win_off[i];
-    for (int j = 0; j < n; ++j) c += wr[j].x >= 0;
-  }
-  n_out[i] = (c + WRUN - 1) / WRUN;
+// Work items: one per used window, grouped into NBUCKET column-range buckets
+// (bucket = c0 * NBUCKET / ncols) so the dynamic ticket order sweeps B's
+// columns once.
+constexpr int NBUCKET = 64;
+
+__device__ __forceinline__ int win_bucket(int32_t c0, int64_t ncols) {
+  return (int)min((int64_t)NBUCKET - 1, ((int64_t)c0 * NBUCKET) / max(ncols, (int64_t)1));
 }
 
-__global__ void k_win_scatter(int64_t m, const int64_t* __restrict__ a_ptr, const int64_t* __restrict__ span_lo,
-                              const int64_t* __restrict__ span_hi, const int64_t* __restrict__ win_off,
-                              const int2* __restrict__ wins, const int32_t* __restrict__ nwin,
-                              const int64_t* __restrict__ out_off, const int64_t* __restrict__ off,
-                              const int64_t* __restrict__ bm_off, WinRun* __restrict__ work) {
+__global__ void k_win_counts(int64_t m, int64_t ncols, const int64_t* __restrict__ win_off,
+                             const int2* __restrict__ wins, const int32_t* __restrict__ nwin,
+                             unsigned long long* __restrict__ bucket_cnt) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int n = nwin[i];
   if (n <= 0) return;
   const int2* wr = wins + win_off[i];
-  int64_t o = off[i];
-  const int32_t rowcnt = (int32_t)(out_off[i + 1] - out_off[i]);
+  for (int j = 0; j < n; ++j)
+    if (wr[j].x >= 0) atomicAdd(&bucket_cnt[win_bucket(wr[j].x, ncols)], 1ull);
+}
+
+__global__ void k_win_scatter(int64_t m, int64_t ncols, const int64_t* __restrict__ a_ptr,
+                              const int64_t* __restrict__ span_lo, const int64_t* __restrict__ span_hi,
+                              const int64_t* __restrict__ win_off, const int2* __restrict__ wins,
+                              const int32_t* __restrict__ nwin, const int64_t* __restrict__ out_off,
+                              const int64_t* __restrict__ bm_off, unsigned long long* __restrict__ cursor,
+                              WinItem* __restrict__ work) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int n = nwin[i];
+  if (n <= 0) return;
+  const int2* wr = wins + win_off[i];
+  const int64_t rowcnt = out_off[i + 1] - out_off[i];
   const int32_t hi1 = (int32_t)(span_hi[i] + 1);
-  WinRun run;
-  run.out_base = out_off[i];
-  run.bm_base = bm_off ? bm_off[i] : 0;
-  run.lo = (int32_t)span_lo[i];
-  run.pad = 0;
-  run.t0 = a_ptr[i];
-  run.t_len = (int32_t)(a_ptr[i + 1] - a_ptr[i]);
-  run.nw = 0;
-  run.first = 1;
-  for (int j = 0; j <= n; ++j) {
-    const bool at_end = j == n;
-    if (!at_end && wr[j].x < 0) continue;
-    const int32_t c = at_end ? hi1 : wr[j].x;
-    const int32_t r = at_end ? rowcnt : wr[j].y;
-    if (run.nw == WRUN || at_end) {
-      // close the run at boundary (c, r)
-      if (run.nw > 0) {
-        run.cb[run.nw] = c;
-        run.rk[run.nw] = r;
-        run.last = at_end ? 1 : 0;
-        work[o++] = run;
-        run.first = 0;
-        run.nw = 0;
-      }
-    }
-    if (!at_end) {
-      run.cb[run.nw] = c;
-      run.rk[run.nw] = r;
-      run.nw++;
-    }
+  const int64_t org = win_origin(span_lo[i]);
+  int j = 0;
+  while (j < n && wr[j].x < 0) ++j;
+  while (j < n) {
+    const int2 me = wr[j];
+    int k = j + 1;
+    while (k < n && wr[k].x < 0) ++k;
+    WinItem it;
+    it.c0 = me.x;
+    it.c1 = k < n ? wr[k].x : hi1;
+    it.last = k < n ? 0 : 1;
+    it.cnt = (int32_t)((k < n ? (int64_t)wr[k].y : rowcnt) - me.y);
+    it.out_base = out_off[i] + me.y;
+    it.t0 = a_ptr[i];
+    it.t_len = (int32_t)(a_ptr[i + 1] - a_ptr[i]);
+    it.bm_word = bm_off ? bm_off[i] + ((int64_t)me.x - org) / 64 : -1;
+    it.pad = 0;
+    const unsigned long long slot = atomicAdd(&cursor[win_bucket(me.x, ncols)], 1ull);
+    work[slot] = it;
+    j = k;
   }
+}
+
+// B tile index: row-length histogram (log2 classes) to pick which rows get a
+// table within the memory budget, then one warp per indexed row walks its
+// columns once and records the tile boundaries.
+__global__ void k_brow_hist(int64_t k, const int64_t* __restrict__ b_ptr, unsigned long long* __restrict__ hist) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  const int64_t len = b_ptr[i + 1] - b_ptr[i];
+  if (len > 0) atomicAdd(&hist[63 - __clzll((unsigned long long)len)], 1ull);
+}
+
+__global__ void k_btile_flags(int64_t k, const int64_t* __restrict__ b_ptr, int64_t min_len, int64_t per_row,
+                              int64_t* __restrict__ sizes) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  sizes[i] = (b_ptr[i + 1] - b_ptr[i] >= min_len) ? per_row : 0;
+}
+
+__global__ void k_btile_build(int64_t k, const int64_t* __restrict__ b_ptr, const int32_t* __restrict__ b_col,
+                              int64_t ntiles, const int64_t* __restrict__ tbl_scan, int64_t* __restrict__ tbl_off,
+                              int32_t* __restrict__ tbl) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = lane_id();
+  if (row >= k) return;
+  const bool has = tbl_scan[row + 1] > tbl_scan[row];
+  if (lane == 0) tbl_off[row] = has ? tbl_scan[row] : -1;
+  if (!has) return;
+  int32_t* t = tbl + tbl_scan[row];
+  const int64_t s = b_ptr[row], len = b_ptr[row + 1] - s;
+  int prev = -1;  // tile of the previous element (warp-uniform after each step)
+  for (int64_t j0 = 0; j0 < len; j0 += 32) {
+    const int64_t j = j0 + lane;
+    const int tj = j < len ? (int)(b_col[s + j] / TILE_COLS) : (int)ntiles;
+    int tp = __shfl_up_sync(SG_FULL, tj, 1);
+    if (lane == 0) tp = prev;
+    // element j is the first column >= t*TILE_COLS for every t in (tp, tj]
+    if (j < len)
+      for (int x = tp + 1; x <= tj; ++x) t[x] = (int32_t)j;
+    const int last_lane = (int)min((int64_t)31, len - 1 - j0);
+    prev = __shfl_sync(SG_FULL, tj, last_lane);
+  }
+  // tiles after the row's last column point past the end
+  if (prev < ntiles)
+    for (int x = prev + 1 + lane; x <= ntiles; x += 32) t[x] = (int32_t)len;
 }
 
 __global__ void k_win_capacity(int64_t m, const int64_t* __restrict__ products, const int64_t* __restrict__ lo,
@@ -1328,7 +1388,7 @@ __global__ void k_win_capacity(int64_t m, const int64_t* __restrict__ products, 
   // fallback count pass (select given): every selected long row
   const bool sel = select == nullptr ? count_uses_bitmap(p, span) : (select[i] && p > 256);
   cap[i] = sel ? window_capacity(p, span) : 0;
-  if (words) words[i] = sel ? (span + 63) / 64 : 0;
+  if (words) words[i] = sel ? (hi[i] - win_origin(lo[i])) / 64 + 1 : 0;
 }
 
 // -------------------------------------------------------------------------
@@ -1501,7 +1561,7 @@ static int launch_bm(const Launch& L, const int32_t* rows, int64_t n) {
   int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 32);
   kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.lo, L.hi, L.out_off, L.out_col,
                            (V*)L.out_val, L.counts, L.overflow,
-                           MODE == 0 ? L.win : Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
+                           MODE == 0 ? L.win : Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
   return check_cuda("k_bitmap");
 }
 
@@ -1570,10 +1630,11 @@ using namespace sg;
 extern "C" {
 
 static Win to_win(const sg_windows_t* w) {
-  if (!w) return Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (!w) return Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   const bool sv = w->bm_save != nullptr && w->pre_save != nullptr;
   return Win{w->win_off, reinterpret_cast<int2*>(w->wins), w->nwin, w->bm_off,
-             sv ? reinterpret_cast<unsigned long long*>(w->bm_save) : nullptr, sv ? w->pre_save : nullptr};
+             sv ? reinterpret_cast<unsigned long long*>(w->bm_save) : nullptr, sv ? w->pre_save : nullptr,
+             w->btile_off, w->btile};
 }
 
 int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col, const int64_t* b_ptr,
@@ -1672,50 +1733,111 @@ int sg_window_capacity(int64_t m, const int64_t* products, const int64_t* span_l
   return SG_OK;
 }
 
-int sg_window_numeric(int64_t m, int dtype, const int64_t* a_ptr, const int32_t* a_col, const void* a_val,
-                      const int64_t* b_ptr, const int32_t* b_col, const void* b_val, const int64_t* span_lo,
-                      const int64_t* span_hi, const sg_windows_t* win, const int64_t* out_off, int32_t* out_col,
-                      void* out_val, void* work_buf, int64_t work_cap, void* ws, size_t ws_bytes, void* stream) {
+int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, const int32_t* a_col,
+                      const void* a_val, const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
+                      const int64_t* span_lo, const int64_t* span_hi, const sg_windows_t* win,
+                      const int64_t* out_off, int32_t* out_col, void* out_val, void* work_buf, int64_t work_cap,
+                      void* ws, size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   if (m == 0 || win == nullptr) return SG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const Win W = to_win(win);
-  k_win_counts<<<grid_for(m, 256), 256, 0, s>>>(m, W.off, W.wins, W.nwin, w.tmp);
+  // bucket histogram (column-range groups), exclusive offsets -> cursors
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(w.bincnt);
+  cudaMemsetAsync(cnt, 0, NBUCKET * sizeof(unsigned long long), s);
+  k_win_counts<<<grid_for(m, 256), 256, 0, s>>>(m, b_ncols, W.off, W.wins, W.nwin, cnt);
   if (int rc = check_cuda("k_win_counts")) return rc;
-  if (int rc = scan_i64(m, w.tmp, w.tmp, w.partials, s)) return rc;
-  int64_t nwork = 0;
-  cudaMemcpyAsync(&nwork, w.tmp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  unsigned long long h[NBUCKET];
+  cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric sync", 0);
+  int64_t nwork = 0;
+  unsigned long long cur[NBUCKET];
+  for (int i = 0; i < NBUCKET; ++i) {
+    cur[i] = (unsigned long long)nwork;
+    nwork += (int64_t)h[i];
+  }
   if (nwork == 0) return SG_OK;
   if (nwork > work_cap) {
     set_error("sg_window_numeric: work buffer too small");
     return SG_ERR_WORKSPACE;
   }
-  WinRun* work = reinterpret_cast<WinRun*>(work_buf);
-  k_win_scatter<<<grid_for(m, 256), 256, 0, s>>>(m, a_ptr, span_lo, span_hi, W.off, W.wins, W.nwin, out_off,
-                                                 w.tmp, W.bm_save ? W.bm_off : nullptr, work);
+  cudaMemcpyAsync(cnt, cur, sizeof(cur), cudaMemcpyHostToDevice, s);
+  WinItem* work = reinterpret_cast<WinItem*>(work_buf);
+  k_win_scatter<<<grid_for(m, 256), 256, 0, s>>>(m, b_ncols, a_ptr, span_lo, span_hi, W.off, W.wins, W.nwin,
+                                                 out_off, W.bm_save ? W.bm_off : nullptr, cnt, work);
   if (int rc = check_cuda("k_win_scatter")) return rc;
-  unsigned long long* ticket = reinterpret_cast<unsigned long long*>(w.bincnt);
-  cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s);
-  constexpr size_t sm = bmr_smem();
-  const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
-  const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms());
   if (W.bm_save) {
     k_expand<<<(int)std::min<int64_t>(m, (int64_t)num_sms() * 16), EXP_NT, 0, s>>>(
         m, W.nwin, W.bm_off, W.bm_save, W.pre_save, span_lo, out_off, out_col);
     if (int rc = check_cuda("k_expand")) return rc;
   }
+  // the ticket lives after the bucket cursors (host copy above must finish first)
+  unsigned long long* ticket = cnt + NBUCKET;
+  cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s);
+  constexpr size_t sm = bmr_smem();
+  const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
+  const BTile bt{W.btile_off, W.btile};
+  const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms());
   if (dtype == SG_F64) {
     auto kern = k_bmr<double>;
     if (int rc = set_smem(kern, sm)) return rc;
-    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, W.bm_save, W.pre_save, out_col, (double*)out_val, ticket);
+    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, bt, W.bm_save, W.pre_save, out_col, (double*)out_val,
+                                  ticket);
   } else {
     auto kern = k_bmr<float>;
     if (int rc = set_smem(kern, sm)) return rc;
-    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, W.bm_save, W.pre_save, out_col, (float*)out_val, ticket);
+    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, bt, W.bm_save, W.pre_save, out_col, (float*)out_val, ticket);
   }
-  return check_cuda("k_bmr");
+  if (int rc = check_cuda("k_bmr")) return rc;
+  // `cur` (host) is read by the async copy above: keep it alive until done
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric end", 0);
+  return SG_OK;
+}
+
+int sg_btile_plan(int64_t k, int64_t b_ncols, const int64_t* b_ptr, int64_t budget_bytes, int64_t* tbl_scan,
+                  int64_t* totals_host, void* ws, size_t ws_bytes, void* stream) {
+  Workspace w;
+  if (!carve(ws, ws_bytes, k, w)) return SG_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ntiles = (b_ncols + TILE_COLS - 1) / TILE_COLS;
+  const int64_t per_row = ntiles + 1;
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(w.bincnt);
+  cudaMemsetAsync(hist, 0, 64 * sizeof(unsigned long long), s);
+  if (k > 0) {
+    k_brow_hist<<<grid_for(k, 256), 256, 0, s>>>(k, b_ptr, hist);
+    if (int rc = check_cuda("k_brow_hist")) return rc;
+  }
+  unsigned long long hh[64];
+  cudaMemcpyAsync(hh, hist, sizeof(hh), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_btile_plan sync", 0);
+  // smallest power-of-two length class (>= 32) whose rows fit the budget
+  int cls = 63;
+  int64_t rows = 0;
+  for (int c = 63; c >= 5; --c) {
+    if ((rows + (int64_t)hh[c]) * per_row * 4 > budget_bytes) break;
+    rows += (int64_t)hh[c];
+    cls = c;
+  }
+  const int64_t min_len = (int64_t)1 << cls;
+  if (k > 0) {
+    k_btile_flags<<<grid_for(k, 256), 256, 0, s>>>(k, b_ptr, rows ? min_len : INT64_MAX, per_row, tbl_scan);
+    if (int rc = check_cuda("k_btile_flags")) return rc;
+  }
+  if (int rc = scan_i64(k, tbl_scan, tbl_scan, w.partials, s)) return rc;
+  cudaMemcpyAsync(totals_host, tbl_scan + k, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_btile_plan end", 0);
+  totals_host[1] = rows ? min_len : -1;
+  return SG_OK;
+}
+
+int sg_btile_build(int64_t k, int64_t b_ncols, const int64_t* b_ptr, const int32_t* b_col, const int64_t* tbl_scan,
+                   int64_t* tbl_off, int32_t* tbl, void* stream) {
+  if (k == 0) return SG_OK;
+  const int64_t ntiles = (b_ncols + TILE_COLS - 1) / TILE_COLS;
+  k_btile_build<<<grid_for(k * 32, 256), 256, 0, (cudaStream_t)stream>>>(k, b_ptr, b_col, ntiles, tbl_scan,
+                                                                         tbl_off, tbl);
+  return check_cuda("k_btile_build");
 }
 
 #ifdef SG_PROF

@@ -102,6 +102,13 @@ __device__ __forceinline__ void smem_add(double* p, double v) { atomicAdd(p, v);
 __device__ __forceinline__ void gmem_red(double* p, double v) { atomicAdd(p, v); }
 __device__ __forceinline__ void gmem_red(float* p, float v) { atomicAdd(p, v); }
 
+// Output of C and the saved key bitmaps stream through L2 once: store them
+// evict-first (st.global.cs) so the gathered B rows stay L2-resident.
+__device__ __forceinline__ void st_stream(int32_t* p, int32_t v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(unsigned long long* p, unsigned long long v) { __stcs(p, v); }
+
 __device__ __forceinline__ uint32_t next_pow2_u32(uint32_t x) {
   return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));
 }

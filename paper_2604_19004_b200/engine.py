@@ -86,10 +86,15 @@ class _Ctx:
         self.sp = stream.cuda_stream
         self.ws = None
         self.ws_bytes = 0
+        self._old_ws = []
 
     def workspace(self, m):
+        """Scratch for the stage calls.  A grown workspace never frees the
+        previous one during the call: a caller may still hold its pointer."""
         need = int(_lib.load().sg_workspace_bytes(int(m)))
         if self.ws is None or self.ws_bytes < need:
+            if self.ws is not None:
+                self._old_ws.append(self.ws)
             self.ws = torch.empty(need, dtype=torch.uint8, device=self.device)
             self.ws_bytes = need
         return ptr(self.ws), self.ws_bytes
@@ -147,6 +152,7 @@ class Windows:
     def __init__(self, off, wins, nwin, bm_off, bm_save, pre_save, total):
         self.off, self.wins, self.nwin, self.bm_off, self.total = off, wins, nwin, bm_off, total
         self.bm_save, self.pre_save = bm_save, pre_save
+        self.btile_off = self.btile = None
         self._struct = None
 
     def struct(self):
@@ -155,6 +161,8 @@ class Windows:
         s.bm_off = ptr(self.bm_off) if self.bm_save is not None else None
         s.bm_save = ptr(self.bm_save) if self.bm_save is not None else None
         s.pre_save = ptr(self.pre_save) if self.bm_save is not None else None
+        s.btile_off = ptr(self.btile_off)
+        s.btile = ptr(self.btile)
         self._struct = s  # keep alive for the call
         return s
 
@@ -190,6 +198,26 @@ def windows(ctx: _Ctx, m, products, lo, hi, select) -> Windows:
             except torch.OutOfMemoryError:
                 bm_save = pre_save = None
     return Windows(off, wins, nwin, bm_off, bm_save, pre_save, total)
+
+
+# the B tile index (sg_btile_plan) may use at most this many bytes
+BTILE_BUDGET = 1 << 30
+
+
+def btile(ctx: _Ctx, B: DeviceCsr, win: Windows):
+    """Build the B tile index for the window pass (rows as long as fit)."""
+    k = B.nrows
+    scan_ = ctx.empty(k + 1, torch.int64)
+    totals = (ctypes.c_int64 * 2)()
+    ws, wsb = ctx.workspace(max(k, 1))
+    _lib.call("sg_btile_plan", k, B.ncols, ptr(B.row_ptr), BTILE_BUDGET, ptr(scan_),
+              ctypes.cast(totals, ctypes.c_void_p), ws, wsb, ctx.sp)
+    if totals[0] <= 0:
+        return
+    off = ctx.empty(max(k, 1), torch.int64)
+    tbl = ctx.empty(int(totals[0]), torch.int32)
+    _lib.call("sg_btile_build", k, B.ncols, ptr(B.row_ptr), ptr(B.col_idx), ptr(scan_), ptr(off), ptr(tbl), ctx.sp)
+    win.btile_off, win.btile = off, tbl
 
 
 def alloc_c(ctx: _Ctx, nnz, dtype, win):
@@ -385,9 +413,11 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         nnz_c = int(row_ptr[-1].item()) if m else 0
         C_col, C_val = alloc_c(ctx, nnz_c, dtype, win)
     if win is not None and win.total:
-        work = ctx.empty(15 * win.total, torch.int64)  # <= one 120-byte run per window
-        _lib.call("sg_window_numeric", m, dcode, *Aargs, ptr(span_lo), ptr(span_hi), win.struct(), ptr(row_ptr),
-                  ptr(C_col), ptr(C_val), ptr(work), win.total, ws, wsb, ctx.sp)
+        btile(ctx, B, win)
+        work = ctx.empty(6 * win.total, torch.int64)  # one 48-byte item per window
+        ws, wsb = ctx.workspace(max(m, 1))
+        _lib.call("sg_window_numeric", m, n, dcode, *Aargs, ptr(span_lo), ptr(span_hi), win.struct(),
+                  ptr(row_ptr), ptr(C_col), ptr(C_val), ptr(work), win.total, ws, wsb, ctx.sp)
     rest, n_rest = (fb_rows, n_fb) if win is None else select_fallback(ctx, m, kind, products, overflow, win.nwin)
     if n_rest:
         _lib.call("sg_fallback", 1, n_rest, ptr(rest), n, dcode, *fargs, ptr(row_ptr),
