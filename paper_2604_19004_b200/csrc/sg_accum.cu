@@ -699,15 +699,17 @@ __device__ __forceinline__ int64_t bitmap_prefix(const unsigned long long* bm, i
 }
 
 // Write the column of every set bit of a 64-bit bitmap word, ascending.
+// Plain (L2-allocating) stores: a warp fills each output line over several
+// instructions, and evict-first partial lines would cost DRAM read-fills.
 __device__ __forceinline__ void emit_bits(unsigned long long bits, int32_t colbase, int32_t* __restrict__ out) {
   unsigned lo = (unsigned)bits, hi = (unsigned)(bits >> 32);
   int k = 0;
   while (lo) {
-    st_stream(out + k++, colbase + __ffs(lo) - 1);
+    out[k++] = colbase + __ffs(lo) - 1;
     lo &= lo - 1;
   }
   while (hi) {
-    st_stream(out + k++, colbase + 31 + __ffs(hi));
+    out[k++] = colbase + 31 + __ffs(hi);
     hi &= hi - 1;
   }
 }
@@ -1253,9 +1255,10 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinItem*
 
 // Column expansion of the long rows from the saved key bitmaps and word
 // ranks: C.col_idx[row_ptr[row] + rank .. ] for every set bit, ascending.
-// One block per row (rows without windows are skipped), a word per thread,
-// per-lane bit loop straight to global memory.  (Staged/coalesced and
-// warp-cooperative variants measured slower on R-MAT-20.)
+// One block per row (rows without windows are skipped), four words per
+// thread per step with the loads issued first, per-lane bit loop straight to
+// global memory.  (Block-staged, warp-staged and warp-cooperative variants
+// all measured slower on R-MAT-20: 64-80 ms vs 59 ms.)
 constexpr int EXP_NT = 256;
 
 __global__ void __launch_bounds__(EXP_NT) k_expand(int64_t m, const int32_t* __restrict__ nwin,
@@ -1270,8 +1273,19 @@ __global__ void __launch_bounds__(EXP_NT) k_expand(int64_t m, const int32_t* __r
     const int64_t w0 = bm_off[r], nw = bm_off[r + 1] - w0;
     const int32_t org = (int32_t)win_origin(span_lo[r]);
     int32_t* out = out_col + out_off[r];
-    for (int64_t i = threadIdx.x; i < nw; i += EXP_NT)
-      emit_bits(__ldcs(bm_save + w0 + i), org + (int32_t)(64 * i), out + __ldcs(pre_save + w0 + i));
+    for (int64_t i0 = threadIdx.x; i0 < nw; i0 += 4 * EXP_NT) {
+      unsigned long long bits[4];
+      int32_t pos[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * EXP_NT;
+        bits[u] = i < nw ? __ldcs(bm_save + w0 + i) : 0ull;
+        pos[u] = i < nw ? __ldcs(pre_save + w0 + i) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        emit_bits(bits[u], org + (int32_t)(64 * (i0 + u * EXP_NT)), out + pos[u]);
+    }
   }
 }
 
