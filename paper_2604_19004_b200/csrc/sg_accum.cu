@@ -1619,13 +1619,46 @@ static const int kOrder[] = {BIN_BM0 + 2, BIN_HB0 + 3, BIN_HB0 + 2, BIN_HB0 + 1,
                              BIN_HBN,     BIN_BM0 + 0, BIN_HW0 + 6, BIN_HW0 + 5, BIN_HW0 + 4, BIN_HW0 + 3,
                              BIN_HW0 + 2, BIN_HW0 + 1, BIN_HW0 + 0, BIN_ESC};
 
+// Bins are independent: launch them on a few forked streams so the small
+// bins fill the tail of the big ones, then join back into the caller's stream.
+struct Fork {
+  static constexpr int N = 4;
+  cudaStream_t main;
+  cudaStream_t side[N];
+  cudaEvent_t ev;
+  explicit Fork(cudaStream_t s) : main(s) {
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, s);
+    for (int i = 0; i < N; ++i) {
+      cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking);
+      cudaStreamWaitEvent(side[i], ev, 0);
+    }
+  }
+  cudaStream_t at(int i) const { return side[i % N]; }
+  ~Fork() {
+    for (int i = 0; i < N; ++i) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      cudaEventRecord(e, side[i]);
+      cudaStreamWaitEvent(main, e, 0);
+      cudaEventDestroy(e);
+      cudaStreamDestroy(side[i]);
+    }
+    cudaEventDestroy(ev);
+  }
+};
+
 template <int MODE, typename V>
 static int run_bins(const Launch& L, int64_t m, Workspace& w, const int32_t* rowmap_unused) {
   int64_t cnt[NBINS], off[NBINS + 1];
   if (int rc = partition_rows(m, NBINS, w, cnt, off, L.s)) return rc;
+  Fork f(L.s);
+  int k = 0;
   for (int b : kOrder) {
     if (cnt[b] == 0) continue;
-    if (int rc = launch_bin<MODE, V>(b, L, w.rowlist + off[b], cnt[b])) return rc;
+    Launch Lb = L;
+    Lb.s = f.at(k++);
+    if (int rc = launch_bin<MODE, V>(b, Lb, w.rowlist + off[b], cnt[b])) return rc;
   }
   return SG_OK;
 }
@@ -1711,15 +1744,19 @@ int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, i
   Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, nullptr, nullptr, nullptr, span_lo, span_hi,
            out_off, out_col, out_val, counts, nullptr, s};
   if (mode == 0) L.win = to_win(win);
+  Fork f(s);
+  int kk = 0;
   for (int b : kOrder) {
     if (cnt[b] == 0) continue;
+    Launch Lb = L;
+    Lb.s = f.at(kk++);
     int rc;
     if (mode == 0)
-      rc = launch_bin<0, double>(b, L, mapped + off[b], cnt[b]);
+      rc = launch_bin<0, double>(b, Lb, mapped + off[b], cnt[b]);
     else if (dtype == SG_F64)
-      rc = launch_bin<1, double>(b, L, mapped + off[b], cnt[b]);
+      rc = launch_bin<1, double>(b, Lb, mapped + off[b], cnt[b]);
     else
-      rc = launch_bin<1, float>(b, L, mapped + off[b], cnt[b]);
+      rc = launch_bin<1, float>(b, Lb, mapped + off[b], cnt[b]);
     if (rc) return rc;
   }
   return SG_OK;
