@@ -8,7 +8,8 @@ rows = list(csv.reader(open(sys.argv[1])))
 hdr = None
 agg = collections.defaultdict(lambda: collections.defaultdict(float))
 cnt = collections.Counter()
-units = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6,
+# times normalised to microseconds, bytes to bytes
+units = {"ns": 1e-3, "us": 1.0, "ms": 1e3, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "KB": 1e3, "MB": 1e6, "GB": 1e9,
          "Gbyte": 1e9, "Tbyte": 1e12}
 for r in rows:
     if "Kernel Name" in r:
@@ -22,9 +23,9 @@ for r in rows:
         if d["Metric Name"] == "gpu__time_duration.sum":
             cnt[k] += 1
 tot_t = sum(a["gpu__time_duration.sum"] for a in agg.values())
-print(f"{'ms':>9} {'share':>6} {'DRAM GB':>8} {'GB/s':>7}  kernel")
+print(f"{'ms':>9} {'share':>6} {'DRAM GB':>8} {'GB/s':>7}  kernel  (ncu: serialised, cold cache)")
 for k, a in sorted(agg.items(), key=lambda x: -x[1]["gpu__time_duration.sum"])[:int(sys.argv[2]) if len(sys.argv) > 2 else 15]:
-    t = a["gpu__time_duration.sum"] / 1e3
+    t = a["gpu__time_duration.sum"] / 1e3  # ms
     b = (a["dram__bytes_read.sum"] + a["dram__bytes_write.sum"]) / 1e9
-    print(f"{t:9.2f} {100 * a['gpu__time_duration.sum'] / tot_t:5.1f}% {b:8.2f} {b / max(t, 1e-9) * 1e3:7.0f}  {k} (x{cnt[k]})")
+    print(f"{t:9.3f} {100 * a['gpu__time_duration.sum'] / tot_t:5.1f}% {b:8.2f} {b / max(t, 1e-9) * 1e3:7.0f}  {k} (x{cnt[k]})")
 print(f"total {tot_t / 1e3:.2f} ms")
