@@ -65,6 +65,15 @@ const char* sg_last_error(void);
  * bench.py reports the count inside its timed region). */
 unsigned long long sg_launch_count(void);
 
+/* Per-kernel device timer (measurement only; bench.py's roofline).  Enabling
+ * (or disabling) clears the record; while enabled, the dominant kernels
+ * ("k_bmr", "k_expand", "k_hash_warp", "k_hash_block", "k_bitmap") are
+ * bracketed by CUDA events on their launching stream.  sg_kernel_time
+ * waits for the recorded launches of `name` and returns their summed
+ * duration and count. */
+int sg_kernel_timer(int enable);
+int sg_kernel_time(const char* name, double* total_ms, int64_t* launches);
+
 /* Scratch bytes needed by sg_symbolic / sg_numeric / sg_fallback / sg_scan
  * for a problem with `m` rows of A. */
 size_t sg_workspace_bytes(int64_t m);

@@ -38,6 +38,8 @@ SIGNATURES = {
     "sg_abi_version": (I32, []),
     "sg_last_error": (C.c_char_p, []),
     "sg_launch_count": (C.c_ulonglong, []),
+    "sg_kernel_timer": (I32, [I32]),
+    "sg_kernel_time": (I32, [C.c_char_p, P, P]),
     "sg_workspace_bytes": (SZ, [I64]),
     "sg_row_stats": (I32, [I64, I64, P, P, P, P, P, P, P, P, P]),
     "sg_hll_build": (I32, [I64, P, P, I32, P, P]),

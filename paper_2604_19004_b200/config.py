@@ -107,6 +107,9 @@ class EngineConfig:
     dtype: str | None = None
     return_device: bool = False
     stream: object | None = None
+    # fill RunReport.window_stats (row/product/nnz totals of the rows the
+    # window kernel k_bmr processes; bench.py's roofline), a few reductions
+    window_stats: bool = False
 
     def __post_init__(self):
         if self.registers is not None and self.registers not in PRECISION_FOR:
@@ -145,6 +148,7 @@ class RunReport:
     gflops: float | None = None
     kernel_ms: dict | None = None
     n_gpus: int = 1
+    window_stats: dict | None = None
 
 
 def select_registers(er: float) -> int:

@@ -1551,8 +1551,10 @@ static int launch_hw(const Launch& L, const int32_t* rows, int64_t n) {
   constexpr size_t sm = hw_smem<LOG2T, MODE>();
   auto kern = k_hash_warp<LOG2T, MODE, V>;
   if (int rc = set_smem(kern, sm)) return rc;
+  ktimer_begin(MODE == 0 ? "k_hash_warp:count" : "k_hash_warp", L.s);
   kern<<<grid_for(n, HW_WARPS), HW_WARPS * 32, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.out_off,
                                                          L.out_col, (V*)L.out_val, L.counts, L.overflow);
+  ktimer_end(L.s);
   return check_cuda("k_hash_warp");
 }
 
@@ -1562,8 +1564,10 @@ static int launch_hb(const Launch& L, const int32_t* rows, int64_t n) {
   auto kern = k_hash_block<LOG2T, MODE, V, NT>;
   if (int rc = set_smem(kern, sm)) return rc;
   int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 16);
+  ktimer_begin(MODE == 0 ? "k_hash_block:count" : "k_hash_block", L.s);
   kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.lo, L.hi, L.out_off, L.out_col,
                            (V*)L.out_val, L.counts, L.overflow);
+  ktimer_end(L.s);
   return check_cuda("k_hash_block");
 }
 
@@ -1573,9 +1577,11 @@ static int launch_bm(const Launch& L, const int32_t* rows, int64_t n) {
   auto kern = k_bitmap<BW, MODE, V, NT>;
   if (int rc = set_smem(kern, sm)) return rc;
   int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 32);
+  ktimer_begin(MODE == 0 ? "k_bitmap:count" : "k_bitmap", L.s);
   kern<<<g, NT, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.lo, L.hi, L.out_off, L.out_col,
                            (V*)L.out_val, L.counts, L.overflow,
                            MODE == 0 ? L.win : Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr});
+  ktimer_end(L.s);
   return check_cuda("k_bitmap");
 }
 
@@ -1819,8 +1825,10 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
                                                  out_off, W.bm_save ? W.bm_off : nullptr, cnt, work);
   if (int rc = check_cuda("k_win_scatter")) return rc;
   if (W.bm_save) {
+    ktimer_begin("k_expand", s);
     k_expand<<<(int)std::min<int64_t>(m, (int64_t)num_sms() * 16), EXP_NT, 0, s>>>(
         m, W.nwin, W.bm_off, W.bm_save, W.pre_save, span_lo, out_off, out_col);
+    ktimer_end(s);
     if (int rc = check_cuda("k_expand")) return rc;
   }
   // the ticket lives after the bucket cursors (host copy above must finish first)
@@ -1830,6 +1838,7 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
   const BTile bt{W.btile_off, W.btile};
   const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms());
+  ktimer_begin("k_bmr", s);
   if (dtype == SG_F64) {
     auto kern = k_bmr<double>;
     if (int rc = set_smem(kern, sm)) return rc;
@@ -1840,6 +1849,7 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
     if (int rc = set_smem(kern, sm)) return rc;
     kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, bt, W.bm_save, W.pre_save, out_col, (float*)out_val, ticket);
   }
+  ktimer_end(s);
   if (int rc = check_cuda("k_bmr")) return rc;
   // `cur` (host) is read by the async copy above: keep it alive until done
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric end", 0);

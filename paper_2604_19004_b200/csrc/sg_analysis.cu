@@ -11,7 +11,9 @@
 // All are HBM-bound integer/byte work: coalesced loads, warp/sub-warp per row,
 // grids sized by rows.
 #include <atomic>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "sg_internal.cuh"
 
@@ -21,6 +23,44 @@ static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 static std::atomic<unsigned long long> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+struct KTimed {
+  std::string name;
+  cudaEvent_t a, b;
+};
+static std::mutex g_kt_mu;
+static std::atomic<bool> g_kt_on{false};
+static std::vector<KTimed> g_kt;
+static thread_local int g_kt_open = -1;
+
+bool ktimer_on() { return g_kt_on.load(std::memory_order_relaxed); }
+
+void ktimer_begin(const char* name, cudaStream_t s) {
+  if (!ktimer_on()) return;
+  KTimed t{name, nullptr, nullptr};
+  cudaEventCreate(&t.a);
+  cudaEventCreate(&t.b);
+  cudaEventRecord(t.a, s);
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  g_kt_open = (int)g_kt.size();
+  g_kt.push_back(t);
+}
+
+void ktimer_end(cudaStream_t s) {
+  if (!ktimer_on() || g_kt_open < 0) return;
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  cudaEventRecord(g_kt[g_kt_open].b, s);
+  g_kt_open = -1;
+}
+
+static void ktimer_clear() {
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  for (auto& t : g_kt) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  g_kt.clear();
+}
 
 // ---------------------------------------------------------------------------
 // row statistics: G lanes per A row
@@ -429,6 +469,33 @@ extern "C" {
 
 int sg_abi_version(void) { return 1; }
 unsigned long long sg_launch_count(void) { return g_launches.load(); }
+
+int sg_kernel_timer(int enable) {
+  ktimer_clear();
+  g_kt_on.store(enable != 0);
+  return SG_OK;
+}
+
+int sg_kernel_time(const char* name, double* total_ms, int64_t* launches) {
+  if (!name || !total_ms || !launches) {
+    set_error("sg_kernel_time: bad arguments");
+    return SG_ERR_ARG;
+  }
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  double ms = 0.0;
+  int64_t n = 0;
+  for (auto& t : g_kt) {
+    if (t.name != name) continue;
+    if (cudaEventSynchronize(t.b) != cudaSuccess) return check_cuda("sg_kernel_time", 0);
+    float e = 0.f;
+    if (cudaEventElapsedTime(&e, t.a, t.b) != cudaSuccess) return check_cuda("sg_kernel_time", 0);
+    ms += e;
+    ++n;
+  }
+  *total_ms = ms;
+  *launches = n;
+  return SG_OK;
+}
 const char* sg_last_error(void) { return g_err.c_str(); }
 size_t sg_workspace_bytes(int64_t m) { return workspace_bytes(m < 0 ? 0 : m); }
 

@@ -58,6 +58,13 @@ inline bool carve(void* ws, size_t ws_bytes, int64_t m, Workspace& w) {
 // diagnostic launch counter (sg_launch_count); incremented by check_cuda
 void count_launches(int n);
 
+// per-kernel CUDA-event timer (sg_kernel_timer / sg_kernel_time): when
+// enabled, ktimer_begin/ktimer_end bracket a launch with events recorded on
+// the launching stream; a no-op otherwise
+bool ktimer_on();
+void ktimer_begin(const char* name, cudaStream_t s);
+void ktimer_end(cudaStream_t s);
+
 // returns SG_OK or SG_ERR_CUDA with the message recorded; `launches` is the
 // number of kernels the caller just enqueued
 inline int check_cuda(const char* where, int launches = 1) {

@@ -418,6 +418,14 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         ws, wsb = ctx.workspace(max(m, 1))
         _lib.call("sg_window_numeric", m, n, dcode, *Aargs, ptr(span_lo), ptr(span_hi), win.struct(),
                   ptr(row_ptr), ptr(C_col), ptr(C_val), ptr(work), win.total, ws, wsb, ctx.sp)
+    wstats = None
+    if cfg.window_stats and win is not None:
+        wrow = win.nwin[:m] > 0
+        rl = row_ptr[1:] - row_ptr[:-1]
+        al = A.row_ptr[1:] - A.row_ptr[:-1]
+        wstats = {"rows": int(wrow.sum()), "windows": win.total, "nnz_a": int(al[wrow].sum()),
+                  "products": int(products[wrow].sum()), "nnz_c": int(rl[wrow].sum()),
+                  "saved_bitmaps": win.bm_save is not None}
     rest, n_rest = (fb_rows, n_fb) if win is None else select_fallback(ctx, m, kind, products, overflow, win.nwin)
     if n_rest:
         _lib.call("sg_fallback", 1, n_rest, ptr(rest), n, dcode, *fargs, ptr(row_ptr),
@@ -467,7 +475,7 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         total_products=total_products, bitmap_query=bool(bitmap_query),
         est_mean_rel_err=est_mean, est_std_rel_err=est_std,
         gflops=(2.0 * total_products / (total_ms * 1e-3) / 1e9) if total_ms > 0 else None,
-        kernel_ms=kms)
+        kernel_ms=kms, window_stats=wstats)
     if cfg.return_device:
         return Cd, report
     return Cd.to_host(), report

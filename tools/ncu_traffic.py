@@ -22,6 +22,22 @@ for r in rows:
         agg[k][d["Metric Name"]] += v
         if d["Metric Name"] == "gpu__time_duration.sum":
             cnt[k] += 1
+if "--json" in sys.argv:
+    # per kernel family (template arguments dropped): DRAM bytes and time per launch
+    import json
+    fam = collections.defaultdict(lambda: [0.0, 0.0, 0])
+    for k, a in agg.items():
+        name = k.split("<")[0].replace("void ", "").replace("sg::", "").strip()
+        targs = k.split("<")[1].split(",") if "<" in k else []
+        if name in ("k_hash_warp", "k_hash_block", "k_bitmap") and len(targs) > 1 and targs[1].strip() == "0":
+            name += ":count"  # MODE 0 = counting pass (sg_kernel_time naming)
+        f = fam[name]
+        f[0] += a["dram__bytes_read.sum"] + a["dram__bytes_write.sum"]
+        f[1] += a["gpu__time_duration.sum"]
+        f[2] += cnt[k]
+    print(json.dumps({k: {"dram_bytes_per_launch": v[0] / v[2], "us_per_launch": v[1] / v[2], "launches": v[2]}
+                      for k, v in fam.items()}, indent=1))
+    sys.exit(0)
 tot_t = sum(a["gpu__time_duration.sum"] for a in agg.values())
 print(f"{'ms':>9} {'share':>6} {'DRAM GB':>8} {'GB/s':>7}  kernel  (ncu: serialised, cold cache)")
 for k, a in sorted(agg.items(), key=lambda x: -x[1]["gpu__time_duration.sum"])[:int(sys.argv[2]) if len(sys.argv) > 2 else 15]:
