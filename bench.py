@@ -77,19 +77,34 @@ class Clocks:
         self.proc = None
 
     def start(self):
+        """Starts the sampler and waits for its first sample, so NVML's
+        start-up (which holds driver locks) happens before the timed region."""
+        self.lines = []
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
+        self.reader = threading.Thread(target=self._read, daemon=True)
+        self.reader.start()
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < 10 and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.skip = len(self.lines)  # samples taken before the timed region
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line)
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=5)
+        self.reader.join(timeout=5)
+        out = "".join(self.lines[max(self.skip - 1, 0):])
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():

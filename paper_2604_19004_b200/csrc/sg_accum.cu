@@ -25,6 +25,9 @@
 // prefix-summed over their B-row lengths and every warp walks a contiguous
 // range of products (CREDUX.OR finds segment owners), so a row with one hub
 // B row keeps all warps busy.
+#include <array>
+#include <map>
+#include <mutex>
 #include <algorithm>
 #include <climits>
 
@@ -325,11 +328,161 @@ __device__ __forceinline__ void bitonic_kv(int* keys, double* vals, int n, int g
 }
 
 // -------------------------------------------------------------------------
+// warp register sort of packed (col << LOG2T | slot) words: blocked layout,
+// element e = lane * IPT + i; stages with partner distance < IPT stay in
+// registers, the others exchange with __shfl_xor (no shared-memory traffic)
+
+template <int IPT>
+__device__ __forceinline__ void warp_bitonic_reg(uint32_t (&r)[IPT], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * IPT; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= IPT) {
+        const int lm = j / IPT;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const bool asc = ((lane * IPT + i) & k) == 0;
+          const uint32_t o = __shfl_xor_sync(SG_FULL, r[i], lm);
+          r[i] = (lower == asc) ? min(r[i], o) : max(r[i], o);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const int p = i ^ j;
+          if (p > i) {
+            const bool asc = ((lane * IPT + i) & k) == 0;
+            const uint32_t a = r[i], b = r[p];
+            r[i] = asc ? min(a, b) : max(a, b);
+            r[p] = asc ? max(a, b) : min(a, b);
+          }
+        }
+      }
+    }
+  }
+}
+
+// every column fits next to a LOG2T-bit slot index in 32 bits
+template <int LOG2T>
+__device__ __forceinline__ bool b_ncols_fit_u32(int64_t ncols) {
+  return ncols <= ((int64_t)1 << (32 - LOG2T));
+}
+
+// packs the occupied slots of a warp hash table (keys[T], -1 = empty) to the
+// front of keys as (col << LOG2T | slot), in slot order; returns the count
+template <int LOG2T>
+__device__ __forceinline__ int warp_compact_packed(int* keys, int lane) {
+  constexpr int T = 1 << LOG2T;
+  int n = 0;
+  for (int s0 = 0; s0 < T; s0 += 32) {
+    const int k = keys[s0 + lane];
+    const bool occ = k != -1;
+    const unsigned b = __ballot_sync(SG_FULL, occ);
+    __syncwarp();
+    if (occ) keys[n + __popc(b & lanemask_lt())] = (int)(((uint32_t)k << LOG2T) | (uint32_t)(s0 + lane));
+    n += __popc(b);
+    __syncwarp();
+  }
+  return n;
+}
+
+// sorts the n packed words at keys[0, n) and writes the row: columns and
+// vals[slot] (n <= 32 * IPT)
+template <int IPT, int LOG2T, typename V>
+__device__ __forceinline__ void warp_sort_emit(int* keys, const double* vals, int n, int lane,
+                                               int32_t* __restrict__ oc, V* __restrict__ ov) {
+  uint32_t r[IPT];
+  uint32_t* pk = reinterpret_cast<uint32_t*>(keys);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int e = lane * IPT + i;
+    r[i] = e < n ? pk[e] : 0xFFFFFFFFu;
+  }
+  warp_bitonic_reg<IPT>(r, lane);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int e = lane * IPT + i;
+    if (e < n) pk[e] = r[i];
+  }
+  __syncwarp();
+  // striped (coalesced) emission
+  for (int e = lane; e < n; e += 32) {
+    const uint32_t p = pk[e];
+    st_stream(oc + e, (int32_t)(p >> LOG2T));
+    st_stream(ov + e, (V)vals[p & ((1u << LOG2T) - 1)]);
+  }
+}
+
+// long rows (n > 512): bitonic sort of the packed words in shared memory
+template <int LOG2T, typename V>
+__device__ __forceinline__ void warp_sort_emit_packed_smem(int* keys, const double* vals, int n, int lane,
+                                                           int32_t* __restrict__ oc, V* __restrict__ ov) {
+  uint32_t* pk = reinterpret_cast<uint32_t*>(keys);
+  const int pad = (int)next_pow2_u32((uint32_t)max(n, 1));  // <= T
+  for (int i = n + lane; i < pad; i += 32) pk[i] = 0xFFFFFFFFu;
+  __syncwarp();
+  for (int k = 2; k <= pad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int q = lane; q < (pad >> 1); q += 32) {
+        const int i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+        const int ixj = i | j;
+        const uint32_t a = pk[i], b = pk[ixj];
+        if ((a > b) == ((i & k) == 0)) {
+          pk[i] = b;
+          pk[ixj] = a;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  for (int e = lane; e < n; e += 32) {
+    const uint32_t p = pk[e];
+    st_stream(oc + e, (int32_t)(p >> LOG2T));
+    st_stream(ov + e, (V)vals[p & ((1u << LOG2T) - 1)]);
+  }
+}
+
+// wide-column fallback: compact (key, val) in place and bitonic-sort them in
+// shared memory; returns the count
+template <int T, typename V>
+__device__ __forceinline__ int warp_sort_emit_smem(int* keys, double* vals, int lane, int32_t* __restrict__ oc,
+                                                   V* __restrict__ ov) {
+  int n = 0;
+  for (int s0 = 0; s0 < T; s0 += 32) {
+    const int k = keys[s0 + lane];
+    const double v = vals[s0 + lane];
+    const bool occ = k != -1;
+    const unsigned b = __ballot_sync(SG_FULL, occ);
+    __syncwarp();
+    if (occ) {
+      const int pos = n + __popc(b & lanemask_lt());
+      keys[pos] = k;
+      vals[pos] = v;
+    }
+    n += __popc(b);
+    __syncwarp();
+  }
+  const int pad = (int)next_pow2_u32((uint32_t)max(n, 1));
+  for (int i = n + lane; i < pad; i += 32) keys[i] = INT_MAX;
+  __syncwarp();
+  bitonic_kv(keys, vals, pad, lane, 32, WarpSync{});
+  for (int i = lane; i < n; i += 32) {
+    st_stream(oc + i, keys[i]);
+    st_stream(ov + i, (V)vals[i]);
+  }
+  return n;
+}
+
+// -------------------------------------------------------------------------
 // HW: warp-per-row shared-memory hash
 
 constexpr int HW_WARPS = 4;
 
-template <int MODE>
+// COUNT = false: no running count (the caller counts occupied slots after
+// the row, overflow = count > limit; identical to the running rule)
+template <int MODE, bool COUNT = true>
 struct HashOp {
   int* keys;
   double* vals;
@@ -350,8 +503,10 @@ struct HashOp {
       if (k == -1) {
         const int old = atomicCAS(&keys[s], -1, col);
         if (old == -1) {
-          const int c = atomicAdd(cnt, 1);
-          if ((int64_t)c >= limit) *ovf = 1;
+          if (COUNT) {
+            const int c = atomicAdd(cnt, 1);
+            if ((int64_t)c >= limit) *ovf = 1;
+          }
           if (MODE) smem_add(&vals[s], v);
           return;
         }
@@ -372,7 +527,7 @@ __global__ void __launch_bounds__(HW_WARPS * 32) k_hash_warp(int64_t nbin, const
                                                              const int64_t* alloc, const int64_t* __restrict__ out_off,
                                                              int32_t* __restrict__ out_col, V* __restrict__ out_val,
                                                              int64_t* __restrict__ counts,
-                                                             uint8_t* __restrict__ overflow) {
+                                                             uint8_t* __restrict__ overflow, int64_t B_ncols) {
   constexpr int T = 1 << LOG2T;
   extern __shared__ __align__(16) unsigned char smem[];
   const int w = warp_id(), lane = lane_id();
@@ -398,46 +553,41 @@ __global__ void __launch_bounds__(HW_WARPS * 32) k_hash_warp(int64_t nbin, const
     *ovf = 0;
   }
   __syncwarp();
-  HashOp<MODE> op{keys, vals, cnt, ovf, LOG2T, row_limit(kind, cap, alloc, row)};
+  const int64_t limit = row_limit(kind, cap, alloc, row);
+  HashOp<MODE, false> op{keys, vals, cnt, ovf, LOG2T, limit};
   warp_row<MODE == 1, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, op,
                          MODE ? ovf : nullptr);
   __syncwarp();
+  int occ = 0;
+  for (int s0 = 0; s0 < T; s0 += 32) occ += __popc(__ballot_sync(SG_FULL, keys[s0 + lane] != -1));
   if (MODE == 0) {
-    if (lane == 0) counts[row] = *cnt;
+    if (lane == 0) counts[row] = occ;
     return;
   }
-  if (*ovf) {
+  if (*ovf || (int64_t)occ > limit) {
     if (lane == 0) {
       counts[row] = 0;
       overflow[row] = 1;
     }
     return;
   }
-  // compact occupied slots to the front, in slot order, in place
-  int n = 0;
-  for (int s0 = 0; s0 < T; s0 += 32) {
-    const int k = keys[s0 + lane];
-    const double v = vals[s0 + lane];
-    const bool occ = k != -1;
-    const unsigned b = __ballot_sync(SG_FULL, occ);
-    __syncwarp();
-    if (occ) {
-      const int pos = n + __popc(b & lanemask_lt());
-      keys[pos] = k;
-      vals[pos] = v;
-    }
-    n += __popc(b);
-    __syncwarp();
-  }
-  const int pad = (int)next_pow2_u32((uint32_t)max(n, 1));
-  for (int i = n + lane; i < pad; i += 32) keys[i] = INT_MAX;
-  __syncwarp();
-  bitonic_kv(keys, vals, pad, lane, 32, WarpSync{});
   const int64_t off = out_off[row];
-  for (int i = lane; i < n; i += 32) {
-    st_stream(out_col + off + i, keys[i]);
-    st_stream(out_val + off + i, (V)vals[i]);
+  int n;
+  if (b_ncols_fit_u32<LOG2T>(B_ncols)) {
+    // pack (col << LOG2T | slot) to the front of keys, sort the packed words
+    // in registers, then emit col = p >> LOG2T with vals[slot]
+    n = warp_compact_packed<LOG2T>(keys, lane);
+    const int ipt = (n + 31) >> 5;
+    if (ipt <= 1) warp_sort_emit<1, LOG2T>(keys, vals, n, lane, out_col + off, out_val + off);
+    else if (ipt <= 2) warp_sort_emit<2, LOG2T>(keys, vals, n, lane, out_col + off, out_val + off);
+    else if (ipt <= 4) warp_sort_emit<4, LOG2T>(keys, vals, n, lane, out_col + off, out_val + off);
+    else if (ipt <= 8) warp_sort_emit<8, LOG2T>(keys, vals, n, lane, out_col + off, out_val + off);
+    else if (ipt <= 16) warp_sort_emit<16, LOG2T>(keys, vals, n, lane, out_col + off, out_val + off);
+    else warp_sort_emit_packed_smem<LOG2T>(keys, vals, n, lane, out_col + off, out_val + off);
+  } else {
+    n = -1;
   }
+  if (n < 0) n = warp_sort_emit_smem<T>(keys, vals, lane, out_col + off, out_val + off);
   if (lane == 0) {
     counts[row] = n;
     overflow[row] = 0;
@@ -1544,6 +1694,7 @@ struct Launch {
   uint8_t* overflow;
   cudaStream_t s;
   Win win{nullptr, nullptr, nullptr, nullptr, nullptr};  // count mode: record numeric windows
+  int64_t b_ncols = INT64_MAX;
 };
 
 template <int LOG2T, int MODE, typename V>
@@ -1553,7 +1704,7 @@ static int launch_hw(const Launch& L, const int32_t* rows, int64_t n) {
   if (int rc = set_smem(kern, sm)) return rc;
   ktimer_begin(MODE == 0 ? "k_hash_warp:count" : "k_hash_warp", L.s);
   kern<<<grid_for(n, HW_WARPS), HW_WARPS * 32, sm, L.s>>>(n, rows, L.A, L.B, L.kind, L.cap, L.alloc, L.out_off,
-                                                         L.out_col, (V*)L.out_val, L.counts, L.overflow);
+                                                         L.out_col, (V*)L.out_val, L.counts, L.overflow, L.b_ncols);
   ktimer_end(L.s);
   return check_cuda("k_hash_warp");
 }
@@ -1627,30 +1778,48 @@ static const int kOrder[] = {BIN_BM0 + 2, BIN_HB0 + 3, BIN_HB0 + 2, BIN_HB0 + 1,
 
 // Bins are independent: launch them on a few forked streams so the small
 // bins fill the tail of the big ones, then join back into the caller's stream.
+// Side streams for independent bin launches: created once per device and
+// reused (stream creation per call costs tens of microseconds); each fork
+// waits on the main stream and joins back with events.
 struct Fork {
   static constexpr int N = 4;
   cudaStream_t main;
   cudaStream_t side[N];
-  cudaEvent_t ev;
+  cudaEvent_t ev[N + 1];
+  int used = 0;
   explicit Fork(cudaStream_t s) : main(s) {
-    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    cudaEventRecord(ev, s);
-    for (int i = 0; i < N; ++i) {
-      cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking);
-      cudaStreamWaitEvent(side[i], ev, 0);
+    static std::mutex mu;
+    static std::map<int, std::array<cudaStream_t, N>> streams;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = streams.find(dev);
+      if (it == streams.end()) {
+        std::array<cudaStream_t, N> a;
+        for (int i = 0; i < N; ++i) cudaStreamCreateWithFlags(&a[i], cudaStreamNonBlocking);
+        it = streams.emplace(dev, a).first;
+      }
+      for (int i = 0; i < N; ++i) side[i] = it->second[i];
     }
+    for (int i = 0; i <= N; ++i) cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    cudaEventRecord(ev[N], s);
   }
-  cudaStream_t at(int i) const { return side[i % N]; }
-  ~Fork() {
-    for (int i = 0; i < N; ++i) {
-      cudaEvent_t e;
-      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      cudaEventRecord(e, side[i]);
-      cudaStreamWaitEvent(main, e, 0);
-      cudaEventDestroy(e);
-      cudaStreamDestroy(side[i]);
+  // the i-th launch's stream (the first waits for the main stream lazily)
+  cudaStream_t at(int i) {
+    const int k = i % N;
+    if (k >= used) {
+      cudaStreamWaitEvent(side[k], ev[N], 0);
+      used = k + 1;
     }
-    cudaEventDestroy(ev);
+    return side[k];
+  }
+  ~Fork() {
+    for (int i = 0; i < used; ++i) {
+      cudaEventRecord(ev[i], side[i]);
+      cudaStreamWaitEvent(main, ev[i], 0);
+    }
+    for (int i = 0; i <= N; ++i) cudaEventDestroy(ev[i]);
   }
 };
 
@@ -1658,12 +1827,14 @@ template <int MODE, typename V>
 static int run_bins(const Launch& L, int64_t m, Workspace& w, const int32_t* rowmap_unused) {
   int64_t cnt[NBINS], off[NBINS + 1];
   if (int rc = partition_rows(m, NBINS, w, cnt, off, L.s)) return rc;
+  int nonempty = 0;
+  for (int b : kOrder) nonempty += cnt[b] != 0;
   Fork f(L.s);
   int k = 0;
   for (int b : kOrder) {
     if (cnt[b] == 0) continue;
     Launch Lb = L;
-    Lb.s = f.at(k++);
+    Lb.s = nonempty > 1 ? f.at(k++) : L.s;
     if (int rc = launch_bin<MODE, V>(b, Lb, w.rowlist + off[b], cnt[b])) return rc;
   }
   return SG_OK;
@@ -1702,7 +1873,7 @@ int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t*
   Launch L{{a_ptr, a_col, nullptr}, {b_ptr, b_col, nullptr}, nullptr, nullptr, nullptr, span_lo, span_hi,
            nullptr, nullptr, nullptr, counts, nullptr, s};
   L.win = to_win(win);
-  (void)b_ncols;
+  L.b_ncols = b_ncols;
   return run_bins<0, double>(L, m, w, nullptr);
 }
 
@@ -1722,6 +1893,7 @@ int sg_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, cons
   if (int rc = check_cuda("k_classify_numeric")) return rc;
   Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, kind, cap, alloc, span_lo, span_hi,
            out_off, out_col, out_val, counts, overflow, s};
+  L.b_ncols = b_ncols;
   if (dtype == SG_F64) return run_bins<1, double>(L, m, w, nullptr);
   if (dtype == SG_F32) return run_bins<1, float>(L, m, w, nullptr);
   set_error("sg_numeric: bad dtype");
@@ -1736,7 +1908,6 @@ int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, i
   Workspace w;
   if (!carve(ws, ws_bytes, nrows, w)) return SG_ERR_WORKSPACE;
   if (nrows == 0) return SG_OK;
-  (void)b_ncols;
   (void)products;
   cudaStream_t s = (cudaStream_t)stream;
   k_classify_fallback<<<grid_for(nrows, 256), 256, 0, s>>>(nrows, rows, span_lo, span_hi, w.bins);
@@ -1749,13 +1920,16 @@ int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, i
   if (int rc = check_cuda("k_gather_rows")) return rc;
   Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, nullptr, nullptr, nullptr, span_lo, span_hi,
            out_off, out_col, out_val, counts, nullptr, s};
+  L.b_ncols = b_ncols;
   if (mode == 0) L.win = to_win(win);
+  int nonempty = 0;
+  for (int b : kOrder) nonempty += cnt[b] != 0;
   Fork f(s);
   int kk = 0;
   for (int b : kOrder) {
     if (cnt[b] == 0) continue;
     Launch Lb = L;
-    Lb.s = f.at(kk++);
+    Lb.s = nonempty > 1 ? f.at(kk++) : s;
     int rc;
     if (mode == 0)
       rc = launch_bin<0, double>(b, Lb, mapped + off[b], cnt[b]);

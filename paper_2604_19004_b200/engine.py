@@ -63,6 +63,21 @@ def sample_rows(nrows: int, ratio: float, min_n: int, max_n: int, seed: int) -> 
     return np.sort(rng.choice(nrows, size=n, replace=False)).astype(np.int64)
 
 
+_SAMPLE_CACHE: dict = {}
+
+
+def sample_rows_device(device, nrows, ratio, min_n, max_n, seed):
+    """sample_rows uploaded once per (device, draw) and reused across calls."""
+    key = (str(device), nrows, ratio, min_n, max_n, seed)
+    t = _SAMPLE_CACHE.get(key)
+    if t is None:
+        if len(_SAMPLE_CACHE) >= 16:
+            _SAMPLE_CACHE.pop(next(iter(_SAMPLE_CACHE)))
+        t = torch.from_numpy(sample_rows(nrows, ratio, min_n, max_n, seed)).to(device)
+        _SAMPLE_CACHE[key] = t
+    return t
+
+
 def tiers_struct(t: TierConfig) -> _lib.SgTiers:
     s = _lib.SgTiers()
     s.n_hash = len(t.hash_capacities)
@@ -130,7 +145,10 @@ def hll_build(ctx: _Ctx, B: DeviceCsr, p: int):
 
 def hll_estimate(ctx: _Ctx, A: DeviceCsr, regs, p: int, rows=None):
     m = 1 << p
-    lin = torch.from_numpy(lin_table(m)).to(ctx.device)
+    key = ("lin", str(ctx.device), m)
+    lin = _SAMPLE_CACHE.get(key)
+    if lin is None:
+        lin = _SAMPLE_CACHE[key] = torch.from_numpy(lin_table(m)).to(ctx.device)
     nsel = A.nrows if rows is None else int(rows.numel())
     est = ctx.empty(nsel, torch.float64)
     _lib.call("sg_hll_estimate", nsel, None if rows is None else ptr(rows), ptr(A.row_ptr),
@@ -317,10 +335,11 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         if m == 0:
             cr = (1.0, 1.0, 0.0)
         else:
-            rows_h = sample_rows(m, cfg.sample_ratio, cfg.sample_min, cfg.sample_max, cfg.seed)
-            rows_d = torch.from_numpy(rows_h).to(ctx.device)
-            est_s = hll_estimate(ctx, A, regs, p, rows_d).cpu().numpy()
-            prods = products[rows_d].cpu().numpy().astype(np.float64)
+            rows_d = sample_rows_device(ctx.device, m, cfg.sample_ratio, cfg.sample_min, cfg.sample_max,
+                                        cfg.seed)
+            est_d = hll_estimate(ctx, A, regs, p, rows_d)
+            both = torch.stack((est_d, products[rows_d].to(torch.float64))).cpu().numpy()
+            est_s, prods = both[0], both[1]
             cr_hat = float(prods.sum() / max(1.0, est_s.sum()))
             row_cr = np.where(prods > 0, prods / np.maximum(est_s, 1.0), 1.0)
             cr = (cr_hat, float(row_cr.mean()), float(row_cr.std()))
