@@ -219,6 +219,30 @@ int sg_compact(int64_t m, int dtype, const int64_t* counts, const uint8_t* skip,
                const int64_t* src_off, const int64_t* dst_off, const int32_t* src_col,
                const void* src_val, int32_t* dst_col, void* dst_val, void* stream);
 
+/* ---- canonical CSR construction (the inputs' preparation on the device) */
+
+/* Scratch bytes for sg_coo_to_csr / sg_transpose with `nnz` entries. */
+size_t sg_build_workspace_bytes(int64_t nnz);
+
+/* Replaces csr.from_triplets (csr.py:52-80): canonical CSR (rows ascending,
+ * columns ascending within a row, duplicate coordinates summed in input
+ * order) from nnz device triplets rows[i], cols[i] (int64) and vals[i]
+ * (dtype SG_F64 / SG_F32).  col_out / val_out hold nnz slots; row_ptr holds
+ * nrows + 1; *nnz_out_host receives the unique count.  SG_ERR_ARG for a
+ * coordinate outside [0, nrows) x [0, ncols) or dimensions / nnz beyond the
+ * 32-bit index limit (csr.py:57-63). */
+int sg_coo_to_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                  const void* vals, int dtype, int64_t* row_ptr, int32_t* col_out, void* val_out,
+                  int64_t* nnz_out_host, void* ws, size_t ws_bytes, void* stream);
+
+/* Replaces csr.transpose (csr.py:90-97): exact transpose of a canonical
+ * nrows x ncols CSR into t_ptr[ncols + 1], t_col / t_val[nnz] (canonical,
+ * rows ascending within every column).  Used by the AA^T mode
+ * (engine.py:113-128). */
+int sg_transpose(int64_t nrows, int64_t ncols, const int64_t* row_ptr, const int32_t* col, const void* val,
+                 int dtype, int64_t* t_ptr, int32_t* t_col, void* t_val, void* ws, size_t ws_bytes,
+                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

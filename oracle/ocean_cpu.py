@@ -108,6 +108,19 @@ def triplets_to_csr(nrows, ncols, rows, cols, vals) -> Csr:
     return Csr(nrows, ncols, ptr, (uk % ncols).astype(np.int32), np.add.reduceat(vals, head))
 
 
+def transpose(a: Csr) -> Csr:
+    """Exact transpose (csr.py:90-97): a column-major counting sort; entries
+    of one output row keep ascending source-row order."""
+    a = as_csr(a)
+    nnz = int(a.row_ptr[-1])
+    cnt = np.bincount(np.asarray(a.col_idx[:nnz], np.int64), minlength=a.ncols)
+    ptr = np.zeros(a.ncols + 1, np.int64)
+    ptr[1:] = np.cumsum(cnt)
+    src_row = np.repeat(np.arange(a.nrows, dtype=np.int64), np.diff(a.row_ptr))
+    perm = np.argsort(np.asarray(a.col_idx[:nnz], np.int64), kind="stable")
+    return Csr(a.ncols, a.nrows, ptr, src_row[perm].astype(np.int32), np.asarray(a.values)[perm])
+
+
 # ---------------------------------------------------------------------------
 # L1 primitives (hll.py, expand.py)
 

@@ -30,6 +30,10 @@ def multiply_mode(a, mode, b=None):
             raise ValueError(f"AA requires a square matrix, got {a.nrows}x{a.ncols}")
         return a, a
     if mode == "aat":
+        from .device import DeviceCsr
+        if isinstance(a, DeviceCsr):
+            from .build import transpose_device
+            return a, transpose_device(a)
         return a, transpose(a)
     if mode == "ab":
         if b is None:
@@ -45,5 +49,17 @@ __all__ = [
     "EngineConfig", "WorkflowOverride", "WorkflowKind", "RunReport", "TierConfig", "PlanKind",
     "ResourceLimitError", "DeadlineExceeded", "CudaLibraryError",
     "select_registers", "select_workflow", "cr_variance_bound",
-    "spgemm", "multiply_mode",
+    "spgemm", "multiply_mode", "from_triplets_device", "transpose_device",
 ]
+
+
+def from_triplets_device(*args, **kwargs):
+    """Canonical CSR from triplets on the GPU; see build.from_triplets_device."""
+    from .build import from_triplets_device as f
+    return f(*args, **kwargs)
+
+
+def transpose_device(*args, **kwargs):
+    """Exact transpose on the GPU; see build.transpose_device."""
+    from .build import transpose_device as f
+    return f(*args, **kwargs)

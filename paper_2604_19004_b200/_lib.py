@@ -39,6 +39,9 @@ SIGNATURES = {
     "sg_last_error": (C.c_char_p, []),
     "sg_launch_count": (C.c_ulonglong, []),
     "sg_kernel_timer": (I32, [I32]),
+    "sg_build_workspace_bytes": (SZ, [I64]),
+    "sg_coo_to_csr": (I32, [I64, I64, I64, P, P, P, I32, P, P, P, P, P, SZ, P]),
+    "sg_transpose": (I32, [I64, I64, P, P, P, I32, P, P, P, P, SZ, P]),
     "sg_kernel_time": (I32, [C.c_char_p, P, P]),
     "sg_workspace_bytes": (SZ, [I64]),
     "sg_row_stats": (I32, [I64, I64, P, P, P, P, P, P, P, P, P]),

@@ -124,8 +124,34 @@ def kats():
         json.dump(out, fh, indent=1, sort_keys=True)
 
 
+def build_cases():
+    """csr.from_triplets / csr.transpose goldens (tests/golden/build/): seeded
+    triplets with duplicates, arbitrary order, empty rows and empty input."""
+    out = os.path.join(HERE, "build")
+    os.makedirs(out, exist_ok=True)
+    specs = [(0, 1, 1, 0), (1, 7, 5, 40), (2, 300, 200, 5000), (3, 2000, 70_000, 60_000),
+             (4, 50_000, 3, 200_000), (5, 1, 100_000, 30_000)]
+    for seed, nr, nc, n in specs:
+        rng = np.random.default_rng(1000 + seed)
+        # skewed rows and a small column pool so duplicates are common
+        rows = np.minimum((rng.pareto(1.2, n) * nr / 20).astype(np.int64), nr - 1) if n else np.empty(0, np.int64)
+        cols = rng.integers(0, max(1, min(nc, 4 * max(1, n // max(1, nr)) + 3)), n) * (nc // max(1, min(nc, 4 * max(1, n // max(1, nr)) + 3)))
+        cols = np.minimum(cols, nc - 1).astype(np.int64)
+        vals = rng.uniform(-1.0, 1.0, n)
+        c = sg.from_triplets(nr, nc, rows, cols, vals)
+        t = sg.transpose(c)
+        np.savez_compressed(os.path.join(out, f"triplets{seed}.npz"), shape=np.array([nr, nc], np.int64),
+                            rows=rows, cols=cols, vals=vals, ptr=c.row_ptr, col=c.col_idx, val=c.values,
+                            t_ptr=t.row_ptr, t_col=t.col_idx, t_val=t.values)
+        print("triplets", seed, nr, nc, n, "-> nnz", int(c.row_ptr[-1]))
+
+
 def main():
+    if sys.argv[1:] == ["build"]:
+        build_cases()
+        return
     kats()
+    build_cases()
     # mixed corpus (reference test_acceptance criterion 1 / test_engine)
     for i in range(24):
         a, b = rmg.pair_for_case(100 + i, i)
