@@ -125,9 +125,9 @@ def kats():
 
 
 def build_cases():
-    """csr.from_triplets / csr.transpose goldens (tests/golden/build/): seeded
+    """csr.from_triplets / csr.transpose goldens (tests/golden/csr_build/): seeded
     triplets with duplicates, arbitrary order, empty rows and empty input."""
-    out = os.path.join(HERE, "build")
+    out = os.path.join(HERE, "csr_build")
     os.makedirs(out, exist_ok=True)
     specs = [(0, 1, 1, 0), (1, 7, 5, 40), (2, 300, 200, 5000), (3, 2000, 70_000, 60_000),
              (4, 50_000, 3, 200_000), (5, 1, 100_000, 30_000)]

@@ -1,7 +1,7 @@
 """Canonical CSR construction: from_triplets
 (reference csr.py:52-80) and transpose (csr.py:90-97).
 
-Goldens in tests/golden/build/ were produced by the real reference
+Goldens in tests/golden/csr_build/ were produced by the real reference
 (make_golden.py build_cases).  CPU tests pin the oracle to them; the GPU
 tests (sg_coo_to_csr / sg_transpose through the C ABI) must match: structure
 bit-exact, values within rtol 1e-12 (duplicates are summed in input order;
@@ -15,7 +15,7 @@ import pytest
 
 from oracle import ocean_cpu as oc
 
-BUILD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "build")
+BUILD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "csr_build")
 CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(BUILD, "triplets*.npz")))
 
 
