@@ -265,9 +265,10 @@ __device__ __forceinline__ void block_row(int64_t row, const int64_t* __restrict
       len = b_ptr[k + 1] - bs;
       if (VALUES) av = (double)a_val[t + threadIdx.x];
     }
-    int64_t P, nent64;
-    const int64_t S = block_excl_scan(len, scan_scratch, &P);
-    const int64_t pos = block_excl_scan((int64_t)(len > 0), scan_scratch, &nent64);
+    // one scan of (len << 12 | nonempty): segment starts and compacted slots
+    int64_t tot;
+    const int64_t ex = block_excl_scan((len << 12) | (int64_t)(len > 0), scan_scratch, &tot);
+    const int64_t S = ex >> 12, pos = ex & 4095, P = tot >> 12, nent64 = tot & 4095;
     if (len > 0) {
       E.S[pos] = S;
       E.bs[pos] = bs;
@@ -868,15 +869,21 @@ __device__ __forceinline__ void emit_bits(unsigned long long bits, int32_t colba
 // the window accumulator): a window holds at most WIN_R distinct columns and
 // spans at most WIN_WORDS*64 columns, so its bitmap, rank prefix and values
 // all sit in shared memory.
-constexpr int WIN_WORDS = 4096;  // 262,144 columns
-constexpr int WIN_R = 16384;     // values per window (128 KB fp64)
+// SG_WIN_SPLIT = 2 halves the window (and the CTA) so two window CTAs share
+// an SM and overlap each other's latency-bound phases
+#ifndef SG_WIN_SPLIT
+#define SG_WIN_SPLIT 1
+#endif
+constexpr int WIN_CTAS = SG_WIN_SPLIT;           // window CTAs per SM
+constexpr int WIN_WORDS = 4096 / SG_WIN_SPLIT;   // 262,144 columns (split 1)
+constexpr int WIN_R = 16384 / SG_WIN_SPLIT;      // values per window (128 KB fp64, split 1)
 // Windows start on TILE_COLS-column tiles (absolute), so each selected B
 // row's segment in a window is two lookups in the B tile index (no search).
 constexpr int TILE_COLS = 4096;
 constexpr int TILE_WORDS = TILE_COLS / 64;
 constexpr int WIN_RP = WIN_R - TILE_COLS;  // a tile adds at most TILE_COLS keys
 constexpr int WIN_TILES = WIN_WORDS / TILE_WORDS;
-constexpr int WIN_NT = 1024;
+constexpr int WIN_NT = 1024 / SG_WIN_SPLIT;
 
 // bitmap origin of a windowed row: span_lo rounded down to a tile
 __host__ __device__ __forceinline__ int64_t win_origin(int64_t lo) { return lo & ~(int64_t)(TILE_COLS - 1); }
@@ -1099,9 +1106,10 @@ __device__ __forceinline__ int64_t block_load_range(int64_t t, int64_t t1, int64
     }
     if (VALUES) av = (double)a_val[t + threadIdx.x];
   }
-  int64_t P, n64;
-  const int64_t S = block_excl_scan(len, scr, &P);
-  const int64_t pos = block_excl_scan((int64_t)(len > 0), scr, &n64);
+  // one scan of (len << 12 | nonempty): segment starts and compacted slots
+  int64_t tot;
+  const int64_t ex = block_excl_scan((len << 12) | (int64_t)(len > 0), scr, &tot);
+  const int64_t S = ex >> 12, pos = ex & 4095, P = tot >> 12, n64 = tot & 4095;
   if (len > 0) {
     E.S[pos] = S;
     E.bs[pos] = bs;
@@ -1121,51 +1129,68 @@ __device__ __forceinline__ void block_chunk_products(const Entries& E, int nent,
   warp_products<VALUES, V>(E, nent, min(P, per * w), min(P, per * (w + 1)), b_col, b_val, op);
 }
 
+// The window's key set lives in shared memory as interleaved 32-bit words
+// {bits, rank of the word's first column within the window} (uint2), so a
+// product's rank is one LDS.64 + POPC; operations use 32-bit shared
+// addresses (no generic-pointer conversions in the inner loop).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(a));
+  return r;
+}
+
+__device__ __forceinline__ void sts_u4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+
+// fp64 add into shared memory: ptxas lowers it to LDS + DADD +
+// ATOMS.CAST.SPIN.64 (store-conditional; no old value returned)
+__device__ __forceinline__ void smem_add_f64(uint32_t a, double v) {
+  asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
 struct WinSetOp {
-  unsigned* bm32;
+  uint32_t wp;  // shared address of the uint2 words
   int32_t c0;
   __device__ __forceinline__ void operator()(int32_t col, double) {
     const uint32_t x = (uint32_t)(col - c0);
-    atomicOr(bm32 + (x >> 5), 1u << (x & 31));
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(wp + (x >> 5) * 8), "r"(1u << (x & 31)) : "memory");
   }
 };
 
 struct WinAddOp {
-  const unsigned long long* bm;
-  const int* pre;
-  double* vals;
+  uint32_t wp;    // shared address of the uint2 words
+  uint32_t vals;  // shared address of the fp64 values
   int32_t c0;
   __device__ __forceinline__ void operator()(int32_t col, double v) {
     const uint32_t x = (uint32_t)(col - c0);
-    const uint32_t w = x >> 6;
 #if defined(SG_PASS2_MODE) && SG_PASS2_MODE == 4
     // experiment: loads only (no rank, no accumulate)
-    if (v == 12345.678) vals[w & 15] = v;
+    if (v == 12345.678) smem_add_f64(vals + (x & 15) * 8, v);
     return;
 #endif
-    const int r = pre[w] + __popcll(bm[w] & ((2ull << (x & 63)) - 1ull)) - 1;
-#if defined(SG_PASS2_MODE) && SG_PASS2_MODE == 3
-    vals[r] += v;  // experiment: racy plain add (wrong values, timing only)
-#else
-    smem_add(&vals[r], v);
-#endif
+    const uint2 p = lds_u2(wp + (x >> 5) * 8);
+    const uint32_t r = p.y + __popc(p.x & ((2u << (x & 31)) - 1u)) - 1u;
+    smem_add_f64(vals + r * 8, v);
   }
 };
 
-// Exclusive popcount prefix over nwords <= WIN_WORDS words in one pass: each
-// lane owns up to 4 consecutive words of its warp's contiguous range.
-__device__ __forceinline__ void window_prefix(const unsigned long long* bm, int* pre, int nwords, int64_t* scr) {
+// Exclusive popcount prefix over n32 <= 2 * WIN_WORDS interleaved words in
+// one pass: each lane owns up to 8 consecutive words of its warp's range.
+__device__ __forceinline__ void window_prefix32(uint2* wp, int n32, int64_t* scr) {
   constexpr int NW = WIN_NT / 32;
   const int w = warp_id(), lane = lane_id();
-  const int per = (nwords + NW - 1) / NW;
-  const int L = (per + 31) / 32;  // words per lane (<= 4 for WIN_WORDS = 4096)
-  const int wb = min(nwords, per * w), we = min(nwords, per * (w + 1));
-  int c[4] = {0, 0, 0, 0};
+  const int per = (n32 + NW - 1) / NW;
+  const int L = (per + 31) / 32;  // <= 8
+  const int wb = min(n32, per * w), we = min(n32, per * (w + 1));
+  int c[8];
   int s = 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 8; ++i) {
     const int idx = wb + lane * L + i;
-    if (i < L && idx < we) c[i] = __popcll(bm[idx]);
+    c[i] = (i < L && idx < we) ? __popc(wp[idx].x) : 0;
     s += c[i];
   }
   const int inc = warp_incl_scan(s);
@@ -1173,12 +1198,20 @@ __device__ __forceinline__ void window_prefix(const unsigned long long* bm, int*
   const int64_t wbase = block_excl_scan(lane == 31 ? (int64_t)inc : (int64_t)0, scr, &tot);
   int run = (int)__shfl_sync(SG_FULL, wbase, 31) + inc - s;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 8; ++i) {
     const int idx = wb + lane * L + i;
-    if (i < L && idx < we) pre[idx] = run;
+    if (i < L && idx < we) wp[idx].y = (uint32_t)run;
     run += c[i];
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ void emit_bits32_smem(uint32_t bits, int32_t colbase, int* __restrict__ out) {
+  int k = 0;
+  while (bits) {
+    out[k++] = colbase + __ffs(bits) - 1;
+    bits &= bits - 1;
+  }
 }
 
 __device__ __forceinline__ void emit_bits_smem(unsigned long long bits, int32_t colbase, int* __restrict__ out) {
@@ -1276,9 +1309,10 @@ __device__ __forceinline__ int64_t block_load_tiles(int64_t t, int64_t t1, int32
     }
     if (VALUES) av = (double)a_val[t + threadIdx.x];
   }
-  int64_t P, n64;
-  const int64_t S = block_excl_scan(len, scr, &P);
-  const int64_t pos = block_excl_scan((int64_t)(len > 0), scr, &n64);
+  // one scan of (len << 12 | nonempty): segment starts and compacted slots
+  int64_t tot;
+  const int64_t ex = block_excl_scan((len << 12) | (int64_t)(len > 0), scr, &tot);
+  const int64_t S = ex >> 12, pos = ex & 4095, P = tot >> 12, n64 = tot & 4095;
   if (len > 0) {
     E.S[pos] = S;
     E.bs[pos] = bs;
@@ -1290,7 +1324,7 @@ __device__ __forceinline__ int64_t block_load_tiles(int64_t t, int64_t t1, int32
 }
 
 constexpr size_t bmr_smem() {
-  return (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8 + (size_t)3 * (WIN_NT + 1) * 8;
+  return (size_t)WIN_WORDS * 16 + (size_t)WIN_R * 8 + (size_t)3 * (WIN_NT + 1) * 8;
 }
 
 // One CTA per window (dynamic tickets; items are grouped by column range so
@@ -1298,7 +1332,7 @@ constexpr size_t bmr_smem() {
 // saved key bitmap and word ranks the window needs one value pass: rank =
 // pre[w] + popc(bits below), fp64 add into shared memory, coalesced write.
 template <typename V>
-__global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinItem* __restrict__ work, Csr A, Csr B,
+__global__ void __launch_bounds__(WIN_NT, WIN_CTAS) k_bmr(int64_t nwork, const WinItem* __restrict__ work, Csr A, Csr B,
                                                    BTile bt, const unsigned long long* __restrict__ bm_save,
                                                    const int32_t* __restrict__ pre_save,
                                                    int32_t* __restrict__ out_col, V* __restrict__ out_val,
@@ -1306,12 +1340,12 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinItem*
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int64_t scr[WIN_NT / 32 + 2];
   __shared__ int64_t item_next;
-  unsigned long long* bm = reinterpret_cast<unsigned long long*>(smem);
-  int* pre = reinterpret_cast<int*>(smem + (size_t)WIN_WORDS * 8);
-  double* vals = reinterpret_cast<double*>(smem + (size_t)WIN_WORDS * 12);
-  unsigned char* ebase = smem + (size_t)WIN_WORDS * 12 + (size_t)WIN_R * 8;
+  uint2* wp = reinterpret_cast<uint2*>(smem);  // 2 * WIN_WORDS interleaved {bits, rank}
+  double* vals = reinterpret_cast<double*>(smem + (size_t)WIN_WORDS * 16);
+  unsigned char* ebase = smem + (size_t)WIN_WORDS * 16 + (size_t)WIN_R * 8;
   Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (WIN_NT + 1),
             reinterpret_cast<double*>(ebase) + 2 * (WIN_NT + 1)};
+  const uint32_t wp_s = smem_addr(wp), vals_s = smem_addr(vals);
   const V* av = (const V*)A.val;
   const V* bv = (const V*)B.val;
   if (threadIdx.x == 0) item_next = (int64_t)atomicAdd(ticket, 1ull);
@@ -1322,28 +1356,29 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinItem*
 #endif
   while (b < nwork) {
     const WinItem it = work[b];
-    __syncthreads();  // everyone has read item_next
-    if (threadIdx.x == 0) item_next = (int64_t)atomicAdd(ticket, 1ull);
     const int32_t c0 = it.c0, c1 = it.c1;
     const int cnt = it.cnt;
     const int nwords = (int)(((int64_t)c1 - c0 + 63) >> 6);
     const bool saved = it.bm_word >= 0 && bm_save != nullptr;
     if (saved) {
+      // saved 64-bit word i -> interleaved words 2i, 2i+1 with their ranks
       const unsigned long long* src = bm_save + it.bm_word;
       const int32_t* psrc = pre_save + it.bm_word;
       const int r0 = __ldcs(psrc);
       for (int i = threadIdx.x; i < nwords; i += WIN_NT) {
-        bm[i] = __ldcs(src + i);
-        pre[i] = __ldcs(psrc + i) - r0;
+        const unsigned long long w = __ldcs(src + i);
+        const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
+        const uint32_t p = (uint32_t)(__ldcs(psrc + i) - r0);
+        sts_u4(wp_s + (uint32_t)i * 16, lo, p, hi, p + (uint32_t)__popc(lo));
       }
     } else {
-      for (int i = threadIdx.x; i < nwords; i += WIN_NT) bm[i] = 0ull;
+      for (int i = threadIdx.x; i < nwords; i += WIN_NT) sts_u4(wp_s + (uint32_t)i * 16, 0u, 0u, 0u, 0u);
     }
     for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
     __syncthreads();
     SG_PH(0);
-    WinSetOp so{reinterpret_cast<unsigned*>(bm), c0};
-    WinAddOp ao{bm, pre, vals, c0};
+    WinSetOp so{wp_s, c0};
+    WinAddOp ao{wp_s, vals_s, c0};
     const int64_t t0 = it.t0, t1 = it.t0 + it.t_len;
     const bool single = it.t_len <= WIN_NT;
     int nent = 0;
@@ -1368,9 +1403,12 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinItem*
           __syncthreads();
         }
       }
-      window_prefix(bm, pre, nwords, scr);
+      window_prefix32(wp, 2 * nwords, scr);
       int* colbuf = reinterpret_cast<int*>(vals);
-      for (int i = threadIdx.x; i < nwords; i += WIN_NT) emit_bits_smem(bm[i], c0 + 64 * i, colbuf + pre[i]);
+      for (int i = threadIdx.x; i < 2 * nwords; i += WIN_NT) {
+        const uint2 p = wp[i];
+        emit_bits32_smem(p.x, c0 + 32 * i, colbuf + p.y);
+      }
       __syncthreads();
       for (int i = threadIdx.x; i < cnt; i += WIN_NT) st_stream(out_col + it.out_base + i, colbuf[i]);
       __syncthreads();
@@ -1378,6 +1416,11 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinItem*
       __syncthreads();
     }
     SG_PH(2);
+    // the next ticket's round trip overlaps this window's value pass; it is
+    // published after the pass (item_next was last read before the setup
+    // barrier above)
+    unsigned long long nb = 0;
+    if (threadIdx.x == 0) nb = atomicAdd(ticket, 1ull);
     if (single) {
       block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
       __syncthreads();
@@ -1389,6 +1432,7 @@ __global__ void __launch_bounds__(WIN_NT, 1) k_bmr(int64_t nwork, const WinItem*
       }
     }
     SG_PH(4);
+    if (threadIdx.x == 0) item_next = (int64_t)nb;
     for (int i = threadIdx.x; i < cnt; i += WIN_NT) st_stream(out_val + it.out_base + i, (V)vals[i]);
     __syncthreads();
     SG_PH(5);
@@ -2011,7 +2055,7 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   constexpr size_t sm = bmr_smem();
   const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
   const BTile bt{W.btile_off, W.btile};
-  const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms());
+  const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms() * WIN_CTAS);
   ktimer_begin("k_bmr", s);
   if (dtype == SG_F64) {
     auto kern = k_bmr<double>;

@@ -205,3 +205,18 @@ def test_config_scale_poisson_and_rmat_vs_oracle(gpu):
             np.testing.assert_array_equal(C.row_ptr, ref.row_ptr)
             np.testing.assert_array_equal(C.col_idx, ref.col_idx)
             np.testing.assert_allclose(C.values, ref.values, rtol=1e-12, atol=0)
+
+
+def test_window_pass_without_saved_bitmaps(gpu, monkeypatch):
+    """Long rows when the saved key bitmaps do not fit (BITMAP_SAVE_SHARE = 0):
+    the window kernel rebuilds keys, ranks and columns itself."""
+    from paper_2604_19004_b200 import engine, matgen, spgemm
+    from oracle import ocean_cpu as oc
+    monkeypatch.setattr(engine, "BITMAP_SAVE_SHARE", 0.0)
+    a = matgen.rmat(13)
+    ref, _ = oc.spgemm(a, a)
+    for o in ("symbolic", "estimate"):
+        C, _ = spgemm(a, a, _cfg(o))
+        np.testing.assert_array_equal(C.row_ptr, ref.row_ptr)
+        np.testing.assert_array_equal(C.col_idx, ref.col_idx)
+        np.testing.assert_allclose(C.values, ref.values, rtol=1e-12, atol=0)
