@@ -243,6 +243,24 @@ int sg_transpose(int64_t nrows, int64_t ncols, const int64_t* row_ptr, const int
                  int dtype, int64_t* t_ptr, int32_t* t_col, void* t_val, void* ws, size_t ws_bytes,
                  void* stream);
 
+/* ---- result download (the e2e path) */
+
+/* Copies `bytes` from device memory to pageable host memory after the work
+ * already enqueued on `stream`: the copy engine fills a ring of pinned
+ * 64 MB staging buffers (allocated once per process) while `threads` native
+ * workers (0 = 8) move them into host_dst, taking its page faults in
+ * parallel.  Blocks until done.  Replaces the host copy-out of the reference
+ * result (engine.py:214-215 returns host arrays). */
+int sg_download(void* host_dst, const void* dev_src, size_t bytes, int threads, void* stream);
+
+/* Page-lock (first touching in parallel) / release a page-aligned host range
+ * in 256 MB registrations measured from p.  A destination pinned this way
+ * from its first byte is downloaded by direct DMA (sg_download checks).
+ * Used by the host result pool (device.py) that recycles C's host buffers
+ * across calls. */
+int sg_host_pin(void* p, size_t bytes, int threads);
+int sg_host_unpin(void* p, size_t bytes, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,6 +42,9 @@ SIGNATURES = {
     "sg_build_workspace_bytes": (SZ, [I64]),
     "sg_coo_to_csr": (I32, [I64, I64, I64, P, P, P, I32, P, P, P, P, P, SZ, P]),
     "sg_transpose": (I32, [I64, I64, P, P, P, I32, P, P, P, P, SZ, P]),
+    "sg_download": (I32, [P, P, SZ, I32, P]),
+    "sg_host_pin": (I32, [P, SZ, I32]),
+    "sg_host_unpin": (I32, [P, SZ, I32]),
     "sg_kernel_time": (I32, [C.c_char_p, P, P]),
     "sg_workspace_bytes": (SZ, [I64]),
     "sg_row_stats": (I32, [I64, I64, P, P, P, P, P, P, P, P, P]),

@@ -110,6 +110,9 @@ class EngineConfig:
     # fill RunReport.window_stats (row/product/nnz totals of the rows the
     # window kernel k_bmr processes; bench.py's roofline), a few reductions
     window_stats: bool = False
+    # host results from the recycled pinned pool (device.HOST_POOL): repeated
+    # calls download C by direct DMA with no page faults
+    host_pool: bool = False
 
     def __post_init__(self):
         if self.registers is not None and self.registers not in PRECISION_FOR:

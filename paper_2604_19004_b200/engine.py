@@ -497,7 +497,8 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         kernel_ms=kms, window_stats=wstats)
     if cfg.return_device:
         return Cd, report
-    return Cd.to_host(), report
+    from .device import HOST_POOL
+    return Cd.to_host(HOST_POOL if cfg.host_pool else None), report
 
 
 def ctypes_int64():

@@ -220,3 +220,37 @@ def test_window_pass_without_saved_bitmaps(gpu, monkeypatch):
         np.testing.assert_array_equal(C.row_ptr, ref.row_ptr)
         np.testing.assert_array_equal(C.col_idx, ref.col_idx)
         np.testing.assert_allclose(C.values, ref.values, rtol=1e-12, atol=0)
+
+
+def test_download_large_ragged(gpu):
+    """sg_download (staging ring + native drains) on a ragged 300 MB tensor."""
+    from paper_2604_19004_b200.device import download
+    n = (300 << 20) // 8 + 12345
+    t = torch.arange(n, dtype=torch.int64, device=gpu) * 3 - 7
+    for thr in (1, 3, 16):
+        out = download(t, thr)
+        assert out.dtype == np.int64 and out.shape == (n,)
+        np.testing.assert_array_equal(out[:5], [-7, -4, -1, 2, 5])
+        assert int(out[-1]) == (n - 1) * 3 - 7
+        assert int(out.sum()) == int(t.sum().item())
+
+
+def test_host_pool_results_recycled(gpu):
+    """EngineConfig(host_pool=True): results land in pinned pool buffers that
+    return to the pool when dropped and are reused by the next call."""
+    import gc
+    from paper_2604_19004_b200 import EngineConfig, matgen, spgemm
+    from paper_2604_19004_b200.device import HOST_POOL
+    from oracle import ocean_cpu as oc
+    a = matgen.rmat(14)
+    ref, _ = oc.spgemm(a, a)
+    for _ in range(2):
+        C, _ = spgemm(a, a, EngineConfig(host_pool=True))
+        np.testing.assert_array_equal(C.row_ptr, ref.row_ptr)
+        np.testing.assert_array_equal(C.col_idx, ref.col_idx)
+        np.testing.assert_allclose(C.values, ref.values, rtol=1e-12, atol=0)
+        del C
+        gc.collect()
+    assert HOST_POOL.free, "dropped results should return to the pool"
+    HOST_POOL.release()
+    assert HOST_POOL.total == 0
