@@ -219,6 +219,14 @@ int sg_compact(int64_t m, int dtype, const int64_t* counts, const uint8_t* skip,
                const int64_t* src_off, const int64_t* dst_off, const int32_t* src_col,
                const void* src_val, int32_t* dst_col, void* dst_val, void* stream);
 
+/* Estimation error of per-row predictions (engine.py:218-226, the est-eval
+ * harness cli.py:301-341): over rows with row_ptr[r+1] > row_ptr[r],
+ * rel = |pred[r] - nnz_r| / nnz_r; out3 (host) = {live rows, mean rel,
+ * population std of rel}.  Deterministic two-pass reduction; ws needs
+ * 16 KB + 64 bytes of device scratch. */
+int sg_est_errors(int64_t m, const double* pred, const int64_t* row_ptr, double* out3, void* ws, size_t ws_bytes,
+                  void* stream);
+
 /* ---- canonical CSR construction (the inputs' preparation on the device) */
 
 /* Scratch bytes for sg_coo_to_csr / sg_transpose with `nnz` entries. */

@@ -591,6 +591,16 @@ def spgemm(a, b, workflow: str = "auto", registers=None, tiers=None, coef=None,
                   total_ms=(time.perf_counter() - t0) * 1e3,
                   overflow_row_count=int(len(fb)), nnz_c=nnz, total_products=st.total,
                   bitmap_query=bool(bitmap_query))
+    # estimation error of the per-row predictions (engine.py:218-226)
+    report["est_mean_rel_err"] = report["est_std_rel_err"] = None
+    if pk == "estimated":
+        truth = np.diff(rp)
+        live = truth > 0
+        if live.any():
+            rel = np.abs(pred[live] - truth[live]) / truth[live]
+            report["est_mean_rel_err"], report["est_std_rel_err"] = float(rel.mean()), float(rel.std())
+        else:
+            report["est_mean_rel_err"] = report["est_std_rel_err"] = 0.0
     C = Csr(a.nrows, b.ncols, rp, cc, cv)
     if keep_intermediates:
         return C, report, dict(stats=st, regs=regs, pred=pred, pred_kind=pk, kind=kind,

@@ -43,6 +43,7 @@ SIGNATURES = {
     "sg_coo_to_csr": (I32, [I64, I64, I64, P, P, P, I32, P, P, P, P, P, SZ, P]),
     "sg_transpose": (I32, [I64, I64, P, P, P, I32, P, P, P, P, SZ, P]),
     "sg_download": (I32, [P, P, SZ, I32, P]),
+    "sg_est_errors": (I32, [I64, P, P, P, P, SZ, P]),
     "sg_host_pin": (I32, [P, SZ, I32]),
     "sg_host_unpin": (I32, [P, SZ, I32]),
     "sg_kernel_time": (I32, [C.c_char_p, P, P]),

@@ -461,6 +461,72 @@ __global__ void __launch_bounds__(256) k_compact(int64_t m, const int64_t* __res
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// estimation error of the per-row predictions (engine.py:218-226): over rows
+// with a non-empty C row, rel = |pred - truth| / truth; mean and population
+// std.  Two deterministic passes: fixed per-block partials (grid-stride), then
+// one block folds them in index order.
+
+constexpr int ERR_T = 256;
+constexpr int ERR_BLOCKS = 1024;
+
+template <int PASS>
+__global__ void __launch_bounds__(ERR_T) k_est_err(int64_t m, const double* __restrict__ pred,
+                                                   const int64_t* __restrict__ row_ptr, const double* __restrict__ mean,
+                                                   double* __restrict__ part) {
+  __shared__ double sh[ERR_T / 32][2];
+  double s = 0.0, c = 0.0;
+  const double mu = PASS == 1 ? *mean : 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * ERR_T + threadIdx.x; r < m; r += (int64_t)gridDim.x * ERR_T) {
+    const int64_t t = row_ptr[r + 1] - row_ptr[r];
+    if (t > 0) {
+      const double rel = fabs(pred[r] - (double)t) / (double)t;
+      if (PASS == 0) {
+        s += rel;
+        c += 1.0;
+      } else {
+        s += (rel - mu) * (rel - mu);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(SG_FULL, s, o);
+    c += __shfl_xor_sync(SG_FULL, c, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sh[threadIdx.x >> 5][0] = s;
+    sh[threadIdx.x >> 5][1] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ss = 0.0, cc = 0.0;
+    for (int w = 0; w < ERR_T / 32; ++w) {
+      ss += sh[w][0];
+      cc += sh[w][1];
+    }
+    part[2 * blockIdx.x] = ss;
+    part[2 * blockIdx.x + 1] = cc;
+  }
+}
+
+// out[0] = live rows, out[1] = mean (PASS 0) / out[2] = std (PASS 1)
+template <int PASS>
+__global__ void __launch_bounds__(32) k_est_err_fold(int nb, const double* __restrict__ part, double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0, c = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    s += part[2 * b];
+    c += part[2 * b + 1];
+  }
+  if (PASS == 0) {
+    out[0] = c;
+    out[1] = c > 0 ? s / c : 0.0;
+  } else {
+    out[2] = out[0] > 0 ? sqrt(s / out[0]) : 0.0;
+  }
+}
+
 }  // namespace sg
 
 using namespace sg;
@@ -585,6 +651,30 @@ int sg_select_fallback(int64_t m, const int8_t* kind, const int64_t* products, c
   cudaMemcpyAsync(n_out_host, w.tmp + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_select_fallback sync");
   return check_cuda("sg_select_fallback");
+}
+
+int sg_est_errors(int64_t m, const double* pred, const int64_t* row_ptr, double* out3, void* ws, size_t ws_bytes,
+                  void* stream) {
+  if (m < 0 || !out3) {
+    set_error("sg_est_errors: bad arguments");
+    return SG_ERR_ARG;
+  }
+  if (!ws || ws_bytes < (size_t)ERR_BLOCKS * 16 + 64) {
+    set_error("sg_est_errors: workspace too small");
+    return SG_ERR_WORKSPACE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  double* part = static_cast<double*>(ws);
+  double* dev_out = part + 2 * ERR_BLOCKS;
+  const int nb = (int)std::min<int64_t>(ERR_BLOCKS, std::max<int64_t>(1, (m + ERR_T - 1) / ERR_T));
+  k_est_err<0><<<nb, ERR_T, 0, s>>>(m, pred, row_ptr, nullptr, part);
+  k_est_err_fold<0><<<1, 32, 0, s>>>(nb, part, dev_out);
+  k_est_err<1><<<nb, ERR_T, 0, s>>>(m, pred, row_ptr, dev_out + 1, part);
+  k_est_err_fold<1><<<1, 32, 0, s>>>(nb, part, dev_out);
+  if (int rc = check_cuda("k_est_err", 4)) return rc;
+  cudaMemcpyAsync(out3, dev_out, 3 * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_est_errors sync", 0);
+  return SG_OK;
 }
 
 int sg_compact(int64_t m, int dtype, const int64_t* counts, const uint8_t* skip, const int64_t* src_off,

@@ -473,14 +473,12 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
 
     est_mean = est_std = None
     if cfg.compute_estimation_errors and pred_kind == "estimated":
-        truth = (row_ptr[1:] - row_ptr[:-1]).to(torch.float64)
-        live = truth > 0
-        if bool(live.any()):
-            rel = (pred[live] - truth[live]).abs() / truth[live]
-            rel_h = rel.cpu().numpy()
-            est_mean, est_std = float(rel_h.mean()), float(rel_h.std())
-        else:
-            est_mean, est_std = 0.0, 0.0
+        # engine.py:218-226 on the device (sg_est_errors)
+        out3 = (ctypes.c_double * 3)()
+        scratch = ctx.empty(2 * 1024 + 8, torch.float64)
+        _lib.call("sg_est_errors", m, ptr(pred), ptr(row_ptr), ctypes.cast(out3, ctypes.c_void_p), ptr(scratch),
+                  scratch.numel() * 8, ctx.sp)
+        est_mean, est_std = float(out3[1]), float(out3[2])
 
     Cd = DeviceCsr(m, n, row_ptr, C_col, C_val)
     total_ms = (time.perf_counter() - t0) * 1e3

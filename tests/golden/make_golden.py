@@ -146,12 +146,36 @@ def build_cases():
         print("triplets", seed, nr, nc, n, "-> nnz", int(c.row_ptr[-1]))
 
 
+def est_eval_cases():
+    """cmd_est_eval's per-register records (cli.py:301-341) for golden inputs:
+    FORCE_ESTIMATE with compute_estimation_errors at m = 32 / 64 / 128."""
+    out = {}
+    for name in ["corpus0", "corpus1", "corpus2", "corpus3", "pair03", "pair07", "pair11", "bitmapq"]:
+        d = dict(np.load(os.path.join(HERE, name + ".npz")))
+        mk = lambda k: sg.CsrMatrix(int(d[k + "_shape"][0]), int(d[k + "_shape"][1]), d[k + "_ptr"],  # noqa: E731
+                                    d[k + "_col"], d[k + "_val"])
+        a, b = mk("A"), mk("B")
+        for m in (32, 64, 128):
+            cfg = sg.EngineConfig(workflow=sg.WorkflowOverride.FORCE_ESTIMATE, registers=m,
+                                  compute_estimation_errors=True)
+            _, r = sg.spgemm(a, b, cfg)
+            out[f"{name}/{m}"] = {k: getattr(r, k) for k in ("est_mean_rel_err", "est_std_rel_err",
+                                                             "overflow_row_count", "cr_hat", "cr_true", "nnz_c")}
+    with open(os.path.join(HERE, "est_eval.json"), "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+    print("est_eval", len(out))
+
+
 def main():
     if sys.argv[1:] == ["build"]:
         build_cases()
         return
+    if sys.argv[1:] == ["est_eval"]:
+        est_eval_cases()
+        return
     kats()
     build_cases()
+    est_eval_cases()
     # mixed corpus (reference test_acceptance criterion 1 / test_engine)
     for i in range(24):
         a, b = rmg.pair_for_case(100 + i, i)
