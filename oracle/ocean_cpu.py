@@ -468,7 +468,7 @@ def acc_dense(a, b, rows, lo, width, alloc, out_c, out_v, offs, chunk=1 << 24):
 
 def spgemm(a, b, workflow: str = "auto", registers=None, tiers=None, coef=None,
            sample_ratio=SAMPLE_RATIO, sample_min=SAMPLE_MIN, sample_max=SAMPLE_MAX,
-           seed: int = 0, workers: int = 1, keep_intermediates: bool = False):
+           seed: int = 0, workers: int = 1, keep_intermediates: bool = False, compute_errors: bool = False):
     """Restated ``engine.spgemm`` (engine.py:136-249).
 
     Returns (Csr C, report dict[, intermediates dict]).  ``workflow`` is one of
@@ -593,7 +593,7 @@ def spgemm(a, b, workflow: str = "auto", registers=None, tiers=None, coef=None,
                   bitmap_query=bool(bitmap_query))
     # estimation error of the per-row predictions (engine.py:218-226)
     report["est_mean_rel_err"] = report["est_std_rel_err"] = None
-    if pk == "estimated":
+    if compute_errors and pk == "estimated":
         truth = np.diff(rp)
         live = truth > 0
         if live.any():

@@ -113,6 +113,9 @@ class EngineConfig:
     # host results from the recycled pinned pool (device.HOST_POOL): repeated
     # calls download C by direct DMA with no page faults
     host_pool: bool = False
+    # size hash-counted rows of the symbolic pass by products / conservative
+    # CR; counts stay exact (overfull rows are recounted)
+    assisted_symbolic: bool = True
 
     def __post_init__(self):
         if self.registers is not None and self.registers not in PRECISION_FOR:

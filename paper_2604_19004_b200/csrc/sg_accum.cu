@@ -556,13 +556,13 @@ __global__ void __launch_bounds__(HW_WARPS * 32) k_hash_warp(int64_t nbin, const
   __syncwarp();
   const int64_t limit = row_limit(kind, cap, alloc, row);
   HashOp<MODE, false> op{keys, vals, cnt, ovf, LOG2T, limit};
-  warp_row<MODE == 1, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, op,
-                         MODE ? ovf : nullptr);
+  warp_row<MODE == 1, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, op, ovf);
   __syncwarp();
   int occ = 0;
   for (int s0 = 0; s0 < T; s0 += 32) occ += __popc(__ballot_sync(SG_FULL, keys[s0 + lane] != -1));
   if (MODE == 0) {
-    if (lane == 0) counts[row] = occ;
+    // a full table (assisted sizing underestimated the row): -1 = recount
+    if (lane == 0) counts[row] = *ovf ? -1 : occ;
     return;
   }
   if (*ovf || (int64_t)occ > limit) {
@@ -633,11 +633,10 @@ __global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* 
     }
     __syncthreads();
     HashOp<MODE> op{keys, vals, &cnt, &ovf, LOG2T, row_limit(kind, cap, alloc, row)};
-    block_row<MODE == 1, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, op,
-                            MODE ? &ovf : nullptr);
+    block_row<MODE == 1, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, op, &ovf);
     __syncthreads();
     if (MODE == 0) {
-      if (threadIdx.x == 0) counts[row] = cnt;
+      if (threadIdx.x == 0) counts[row] = ovf ? -1 : cnt;  // -1: recount (assisted sizing)
       __syncthreads();
       continue;
     }
@@ -1627,28 +1626,43 @@ __device__ __forceinline__ int64_t pow2_at_least(int64_t x) {
 }
 
 // mode 0 (symbolic)
+// Assisted symbolic binning: hash rows are sized by
+// products / crc, crc the conservative sampled CR (predict.py:111-118),
+// instead of by products; a row whose table fills is flagged (-1) by the count
+// kernel and recounted with product sizing (rerun = 1 classifies only those).
 __global__ void k_classify_count(int64_t m, const int64_t* __restrict__ products, const int64_t* __restrict__ lo,
                                  const int64_t* __restrict__ hi, uint8_t* __restrict__ bins,
-                                 int64_t* __restrict__ counts) {
+                                 int64_t* __restrict__ counts, double crc, int rerun) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int64_t p = products[i];
   uint8_t b;
-  if (p == 0) {
+  if (rerun && counts[i] >= 0) {
+    b = BIN_NONE;
+  } else if (p == 0) {
     b = BIN_NONE;
     counts[i] = 0;
   } else {
     const int64_t span = hi[i] - lo[i] + 1;
-    const int64_t T = max(pow2_at_least(2 * p), (int64_t)32);
+    const int64_t est = (crc > 1.0 && !rerun) ? max((int64_t)1, (int64_t)ceil((double)p / crc)) : p;
+    const int64_t T = max(pow2_at_least(2 * est), (int64_t)32);
     if (count_uses_bitmap(p, span)) {
       b = bm_bin(span);
-    } else if (p <= 1024) {
+    } else if (est <= 1024) {
       b = (uint8_t)(BIN_HW0 + log2_pow2(T) - 5);
     } else {
       b = (uint8_t)(BIN_HB0 + log2_pow2(max(T, (int64_t)4096)) - 12);
     }
   }
   bins[i] = b;
+}
+
+__global__ void k_count_negative(int64_t m, const int64_t* __restrict__ counts, unsigned long long* __restrict__ n) {
+  int c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    c += counts[i] < 0;
+  c = __reduce_add_sync(SG_FULL, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(n, (unsigned long long)c);
 }
 
 // mode 1 (numeric phase)
@@ -1907,17 +1921,33 @@ static Win to_win(const sg_windows_t* w) {
 
 int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col, const int64_t* b_ptr,
                 const int32_t* b_col, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
-                int64_t* counts, const sg_windows_t* win, void* ws, size_t ws_bytes, void* stream) {
+                int64_t* counts, const sg_windows_t* win, double assist_cr, void* ws, size_t ws_bytes,
+                void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   if (m == 0) return SG_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  k_classify_count<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, w.bins, counts);
+  const double crc = assist_cr > 1.0 ? assist_cr : 1.0;
+  k_classify_count<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, w.bins, counts, crc, 0);
   if (int rc = check_cuda("k_classify_count")) return rc;
   Launch L{{a_ptr, a_col, nullptr}, {b_ptr, b_col, nullptr}, nullptr, nullptr, nullptr, span_lo, span_hi,
            nullptr, nullptr, nullptr, counts, nullptr, s};
   L.win = to_win(win);
   L.b_ncols = b_ncols;
+  if (int rc = run_bins<0, double>(L, m, w, nullptr)) return rc;
+  if (crc == 1.0) return SG_OK;
+  // recount the rows whose assisted table filled up, with product sizing
+  unsigned long long* nneg = reinterpret_cast<unsigned long long*>(w.bincnt) + 120;
+  cudaMemsetAsync(nneg, 0, sizeof(unsigned long long), s);
+  k_count_negative<<<std::min(grid_for(m, 256), num_sms() * 8), 256, 0, s>>>(m, counts, nneg);
+  if (int rc = check_cuda("k_count_negative")) return rc;
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, nneg, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_symbolic sync", 0);
+  if (h == 0) return SG_OK;
+  k_classify_count<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, w.bins, counts, 1.0, 1);
+  if (int rc = check_cuda("k_classify_count")) return rc;
+  L.win = Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // bitmap rows are done
   return run_bins<0, double>(L, m, w, nullptr);
 }
 

@@ -358,8 +358,11 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     if kind_wf is WorkflowKind.SYMBOLIC:
         pred = ctx.empty(m, torch.int64)
         win = windows(ctx, m, products, span_lo, span_hi, None)
+        # assisted symbolic binning with the conservative
+        # sampled CR (predict.py:111-118) when the sample was taken
+        assist = 1.0 if (cr is None or not cfg.assisted_symbolic) else max(1.0, cr[1] - 2.0 * cr[2])
         _lib.call("sg_symbolic", m, n, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
-                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(pred), win.struct(), ws, wsb, ctx.sp)
+                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(pred), win.struct(), assist, ws, wsb, ctx.sp)
         pred_kind = "exact"
     elif kind_wf is WorkflowKind.HLL_ESTIMATION:
         pred = hll_estimate(ctx, A, regs, p)

@@ -29,7 +29,7 @@ def test_oracle_est_errors_match_reference(key):
     from oracle import ocean_cpu as oc
     name, m = key.split("/")
     c = Case(name)
-    _, rep = oc.spgemm(c.A, c.B, workflow="estimate", registers=int(m))
+    _, rep = oc.spgemm(c.A, c.B, workflow="estimate", registers=int(m), compute_errors=True)
     want = GOLD[key]
     assert rep["overflow_row_count"] == want["overflow_row_count"]
     assert rep["nnz_c"] == want["nnz_c"]

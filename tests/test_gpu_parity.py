@@ -82,7 +82,7 @@ def test_stage_kernels_match_reference(gpu, name):
     ws, wsb = ctx.workspace(m)
     exact = torch.empty(m, dtype=torch.int64, device=gpu)
     L.call("sg_symbolic", m, B.ncols, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
-           ptr(products), ptr(lo), ptr(hi), ptr(exact), None, ws, wsb, ctx.sp)
+           ptr(products), ptr(lo), ptr(hi), ptr(exact), None, 1.0, ws, wsb, ctx.sp)
     np.testing.assert_array_equal(exact.cpu().numpy(), c.d["exact"])
     t = c.tiers() or TierConfig()
     est6 = hll_estimate(ctx, A, hll_build(ctx, B, 6), 6)
@@ -254,3 +254,24 @@ def test_host_pool_results_recycled(gpu):
     assert HOST_POOL.free, "dropped results should return to the pool"
     HOST_POOL.release()
     assert HOST_POOL.total == 0
+
+
+@pytest.mark.parametrize("assist", [1.5, 4.0, 64.0])
+def test_assisted_symbolic_counts_exact(gpu, assist):
+    """Assisted symbolic binning: rows sized by
+    products / CR, overfull tables recounted -- counts stay exact even with an
+    absurd CR (64) that overflows most tables."""
+    import paper_2604_19004_b200._lib as L
+    from paper_2604_19004_b200.device import ptr, to_device
+    from paper_2604_19004_b200.engine import _Ctx, row_stats
+    for name in ("pair05", "corpus1", "enhanced", "bitmapq"):
+        c = Case(name)
+        ctx = _Ctx(gpu, torch.cuda.current_stream(gpu))
+        A, B = to_device(c.A, gpu), to_device(c.B, gpu)
+        products, lo, hi, _ = row_stats(ctx, A, B)
+        m = A.nrows
+        ws, wsb = ctx.workspace(m)
+        exact = torch.empty(m, dtype=torch.int64, device=gpu)
+        L.call("sg_symbolic", m, B.ncols, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
+               ptr(products), ptr(lo), ptr(hi), ptr(exact), None, assist, ws, wsb, ctx.sp)
+        np.testing.assert_array_equal(exact.cpu().numpy(), c.d["exact"], err_msg=name)
