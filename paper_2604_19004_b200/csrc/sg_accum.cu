@@ -1178,8 +1178,9 @@ struct WinAddOp {
 
 // Exclusive popcount prefix over n32 <= 2 * WIN_WORDS interleaved words in
 // one pass: each lane owns up to 8 consecutive words of its warp's range.
+template <int NT>
 __device__ __forceinline__ void window_prefix32(uint2* wp, int n32, int64_t* scr) {
-  constexpr int NW = WIN_NT / 32;
+  constexpr int NW = NT / 32;
   const int w = warp_id(), lane = lane_id();
   const int per = (n32 + NW - 1) / NW;
   const int L = (per + 31) / 32;  // <= 8
@@ -1322,28 +1323,34 @@ __device__ __forceinline__ int64_t block_load_tiles(int64_t t, int64_t t1, int32
   return P;
 }
 
+template <int NT, int WORDS, int R>
 constexpr size_t bmr_smem() {
-  return (size_t)WIN_WORDS * 16 + (size_t)WIN_R * 8 + (size_t)3 * (WIN_NT + 1) * 8;
+  return (size_t)WORDS * 16 + (size_t)R * 8 + (size_t)3 * (NT + 1) * 8;
 }
+
+// Small windows (<= R/2 values over <= WORDS/2 words) run in half-size CTAs,
+// two per SM, so one window's latency-bound setup / load phases overlap the
+// other's value pass; the rest run one 1024-thread CTA per SM.
+constexpr int SMALL_NT = WIN_NT / 2, SMALL_WORDS = WIN_WORDS / 2, SMALL_R = WIN_R / 2;
 
 // One CTA per window (dynamic tickets; items are grouped by column range so
 // concurrent CTAs gather the same B-row slabs and keep them in L2).  With the
 // saved key bitmap and word ranks the window needs one value pass: rank =
 // pre[w] + popc(bits below), fp64 add into shared memory, coalesced write.
-template <typename V>
-__global__ void __launch_bounds__(WIN_NT, WIN_CTAS) k_bmr(int64_t nwork, const WinItem* __restrict__ work, Csr A, Csr B,
+template <typename V, int NT, int WORDS, int R, int CTAS>
+__global__ void __launch_bounds__(NT, CTAS) k_bmr(int64_t nwork, const WinItem* __restrict__ work, Csr A, Csr B,
                                                    BTile bt, const unsigned long long* __restrict__ bm_save,
                                                    const int32_t* __restrict__ pre_save,
                                                    int32_t* __restrict__ out_col, V* __restrict__ out_val,
                                                    unsigned long long* __restrict__ ticket) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int64_t scr[WIN_NT / 32 + 2];
+  __shared__ int64_t scr[NT / 32 + 2];
   __shared__ int64_t item_next;
-  uint2* wp = reinterpret_cast<uint2*>(smem);  // 2 * WIN_WORDS interleaved {bits, rank}
-  double* vals = reinterpret_cast<double*>(smem + (size_t)WIN_WORDS * 16);
-  unsigned char* ebase = smem + (size_t)WIN_WORDS * 16 + (size_t)WIN_R * 8;
-  Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (WIN_NT + 1),
-            reinterpret_cast<double*>(ebase) + 2 * (WIN_NT + 1)};
+  uint2* wp = reinterpret_cast<uint2*>(smem);  // 2 * WORDS interleaved {bits, rank}
+  double* vals = reinterpret_cast<double*>(smem + (size_t)WORDS * 16);
+  unsigned char* ebase = smem + (size_t)WORDS * 16 + (size_t)R * 8;
+  Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (NT + 1),
+            reinterpret_cast<double*>(ebase) + 2 * (NT + 1)};
   const uint32_t wp_s = smem_addr(wp), vals_s = smem_addr(vals);
   const V* av = (const V*)A.val;
   const V* bv = (const V*)B.val;
@@ -1364,22 +1371,22 @@ __global__ void __launch_bounds__(WIN_NT, WIN_CTAS) k_bmr(int64_t nwork, const W
       const unsigned long long* src = bm_save + it.bm_word;
       const int32_t* psrc = pre_save + it.bm_word;
       const int r0 = __ldcs(psrc);
-      for (int i = threadIdx.x; i < nwords; i += WIN_NT) {
+      for (int i = threadIdx.x; i < nwords; i += NT) {
         const unsigned long long w = __ldcs(src + i);
         const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
         const uint32_t p = (uint32_t)(__ldcs(psrc + i) - r0);
         sts_u4(wp_s + (uint32_t)i * 16, lo, p, hi, p + (uint32_t)__popc(lo));
       }
     } else {
-      for (int i = threadIdx.x; i < nwords; i += WIN_NT) sts_u4(wp_s + (uint32_t)i * 16, 0u, 0u, 0u, 0u);
+      for (int i = threadIdx.x; i < nwords; i += NT) sts_u4(wp_s + (uint32_t)i * 16, 0u, 0u, 0u, 0u);
     }
-    for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
+    for (int i = threadIdx.x; i < cnt; i += NT) vals[i] = 0.0;
     __syncthreads();
     SG_PH(0);
     WinSetOp so{wp_s, c0};
     WinAddOp ao{wp_s, vals_s, c0};
     const int64_t t0 = it.t0, t1 = it.t0 + it.t_len;
-    const bool single = it.t_len <= WIN_NT;
+    const bool single = it.t_len <= NT;
     int nent = 0;
     int64_t P = 0;
     if (single) {
@@ -1396,22 +1403,22 @@ __global__ void __launch_bounds__(WIN_NT, WIN_CTAS) k_bmr(int64_t nwork, const W
         block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
         __syncthreads();
       } else {
-        for (int64_t t = t0; t < t1; t += WIN_NT) {
+        for (int64_t t = t0; t < t1; t += NT) {
           P = block_load_tiles<false, V>(t, t1, c0, c1, it.last, A.col, av, B.ptr, B.col, bt, E, scr, nent);
           block_chunk_products<false, V>(E, nent, P, B.col, bv, so);
           __syncthreads();
         }
       }
-      window_prefix32(wp, 2 * nwords, scr);
+      window_prefix32<NT>(wp, 2 * nwords, scr);
       int* colbuf = reinterpret_cast<int*>(vals);
-      for (int i = threadIdx.x; i < 2 * nwords; i += WIN_NT) {
+      for (int i = threadIdx.x; i < 2 * nwords; i += NT) {
         const uint2 p = wp[i];
         emit_bits32_smem(p.x, c0 + 32 * i, colbuf + p.y);
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < cnt; i += WIN_NT) st_stream(out_col + it.out_base + i, colbuf[i]);
+      for (int i = threadIdx.x; i < cnt; i += NT) st_stream(out_col + it.out_base + i, colbuf[i]);
       __syncthreads();
-      for (int i = threadIdx.x; i < cnt; i += WIN_NT) vals[i] = 0.0;
+      for (int i = threadIdx.x; i < cnt; i += NT) vals[i] = 0.0;
       __syncthreads();
     }
     SG_PH(2);
@@ -1424,7 +1431,7 @@ __global__ void __launch_bounds__(WIN_NT, WIN_CTAS) k_bmr(int64_t nwork, const W
       block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
       __syncthreads();
     } else {
-      for (int64_t t = t0; t < t1; t += WIN_NT) {
+      for (int64_t t = t0; t < t1; t += NT) {
         P = block_load_tiles<true, V>(t, t1, c0, c1, it.last, A.col, av, B.ptr, B.col, bt, E, scr, nent);
         block_chunk_products<true, V>(E, nent, P, B.col, bv, ao);
         __syncthreads();
@@ -1432,7 +1439,7 @@ __global__ void __launch_bounds__(WIN_NT, WIN_CTAS) k_bmr(int64_t nwork, const W
     }
     SG_PH(4);
     if (threadIdx.x == 0) item_next = (int64_t)nb;
-    for (int i = threadIdx.x; i < cnt; i += WIN_NT) st_stream(out_val + it.out_base + i, (V)vals[i]);
+    for (int i = threadIdx.x; i < cnt; i += NT) st_stream(out_val + it.out_base + i, (V)vals[i]);
     __syncthreads();
     SG_PH(5);
 #ifdef SG_PROF
@@ -1491,16 +1498,39 @@ __device__ __forceinline__ int win_bucket(int32_t c0, int64_t ncols) {
   return (int)min((int64_t)NBUCKET - 1, ((int64_t)c0 * NBUCKET) / max(ncols, (int64_t)1));
 }
 
+// window class: 0 = full CTA, 1 = small (fits a half-size CTA)
+__device__ __forceinline__ int win_class(int64_t cnt, int32_t c0, int32_t c1) {
+  return (cnt <= SMALL_R && ((int64_t)c1 - c0 + 63) / 64 <= SMALL_WORDS) ? 1 : 0;
+}
+
+// walks the used windows of row i: f(c0, c1, last, cnt, rank0)
+template <class F>
+__device__ __forceinline__ void for_each_window(const int2* wr, int n, int64_t rowcnt, int32_t hi1, F f) {
+  int j = 0;
+  while (j < n && wr[j].x < 0) ++j;
+  while (j < n) {
+    const int2 me = wr[j];
+    int k = j + 1;
+    while (k < n && wr[k].x < 0) ++k;
+    const int32_t c1 = k < n ? wr[k].x : hi1;
+    const int64_t cnt = (k < n ? (int64_t)wr[k].y : rowcnt) - me.y;
+    f(me.x, c1, k >= n, cnt, me.y);
+    j = k;
+  }
+}
+
 __global__ void k_win_counts(int64_t m, int64_t ncols, const int64_t* __restrict__ win_off,
                              const int2* __restrict__ wins, const int32_t* __restrict__ nwin,
+                             const int64_t* __restrict__ span_hi, const int64_t* __restrict__ out_off,
                              unsigned long long* __restrict__ bucket_cnt) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int n = nwin[i];
   if (n <= 0) return;
-  const int2* wr = wins + win_off[i];
-  for (int j = 0; j < n; ++j)
-    if (wr[j].x >= 0) atomicAdd(&bucket_cnt[win_bucket(wr[j].x, ncols)], 1ull);
+  for_each_window(wins + win_off[i], n, out_off[i + 1] - out_off[i], (int32_t)(span_hi[i] + 1),
+                  [&](int32_t c0, int32_t c1, bool, int64_t cnt, int32_t) {
+                    atomicAdd(&bucket_cnt[win_class(cnt, c0, c1) * NBUCKET + win_bucket(c0, ncols)], 1ull);
+                  });
 }
 
 __global__ void k_win_scatter(int64_t m, int64_t ncols, const int64_t* __restrict__ a_ptr,
@@ -1513,30 +1543,23 @@ __global__ void k_win_scatter(int64_t m, int64_t ncols, const int64_t* __restric
   if (i >= m) return;
   const int n = nwin[i];
   if (n <= 0) return;
-  const int2* wr = wins + win_off[i];
-  const int64_t rowcnt = out_off[i + 1] - out_off[i];
-  const int32_t hi1 = (int32_t)(span_hi[i] + 1);
   const int64_t org = win_origin(span_lo[i]);
-  int j = 0;
-  while (j < n && wr[j].x < 0) ++j;
-  while (j < n) {
-    const int2 me = wr[j];
-    int k = j + 1;
-    while (k < n && wr[k].x < 0) ++k;
-    WinItem it;
-    it.c0 = me.x;
-    it.c1 = k < n ? wr[k].x : hi1;
-    it.last = k < n ? 0 : 1;
-    it.cnt = (int32_t)((k < n ? (int64_t)wr[k].y : rowcnt) - me.y);
-    it.out_base = out_off[i] + me.y;
-    it.t0 = a_ptr[i];
-    it.t_len = (int32_t)(a_ptr[i + 1] - a_ptr[i]);
-    it.bm_word = bm_off ? bm_off[i] + ((int64_t)me.x - org) / 64 : -1;
-    it.pad = 0;
-    const unsigned long long slot = atomicAdd(&cursor[win_bucket(me.x, ncols)], 1ull);
-    work[slot] = it;
-    j = k;
-  }
+  for_each_window(wins + win_off[i], n, out_off[i + 1] - out_off[i], (int32_t)(span_hi[i] + 1),
+                  [&](int32_t c0, int32_t c1, bool last, int64_t cnt, int32_t rank0) {
+                    WinItem it;
+                    it.c0 = c0;
+                    it.c1 = c1;
+                    it.last = last ? 1 : 0;
+                    it.cnt = (int32_t)cnt;
+                    it.out_base = out_off[i] + rank0;
+                    it.t0 = a_ptr[i];
+                    it.t_len = (int32_t)(a_ptr[i + 1] - a_ptr[i]);
+                    it.bm_word = bm_off ? bm_off[i] + ((int64_t)c0 - org) / 64 : -1;
+                    it.pad = 0;
+                    const unsigned long long slot =
+                        atomicAdd(&cursor[win_class(cnt, c0, c1) * NBUCKET + win_bucket(c0, ncols)], 1ull);
+                    work[slot] = it;
+                  });
 }
 
 // B tile index: row-length histogram (log2 classes) to pick which rows get a
@@ -1909,6 +1932,17 @@ __global__ void k_gather_rows(int64_t n, const int32_t* __restrict__ idx, const 
 
 using namespace sg;
 
+template <typename V, int NT, int WORDS, int R, int CTAS>
+static int launch_bmr(int64_t n, const WinItem* work, const Csr& A, const Csr& B, const BTile& bt, const Win& W,
+                      int32_t* out_col, void* out_val, unsigned long long* ticket, cudaStream_t s) {
+  constexpr size_t sm = bmr_smem<NT, WORDS, R>();
+  auto kern = k_bmr<V, NT, WORDS, R, CTAS>;
+  if (int rc = set_smem(kern, sm)) return rc;
+  const int grid = (int)std::min<int64_t>(n, (int64_t)num_sms() * CTAS);
+  kern<<<grid, NT, sm, s>>>(n, work, A, B, bt, W.bm_save, W.pre_save, out_col, (V*)out_val, ticket);
+  return check_cuda("k_bmr");
+}
+
 extern "C" {
 
 static Win to_win(const sg_windows_t* w) {
@@ -2048,19 +2082,23 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   if (m == 0 || win == nullptr) return SG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const Win W = to_win(win);
-  // bucket histogram (column-range groups), exclusive offsets -> cursors
+  // (class, bucket) histogram -> exclusive offsets -> cursors; the small
+  // class comes first in the work array
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(w.bincnt);
-  cudaMemsetAsync(cnt, 0, NBUCKET * sizeof(unsigned long long), s);
-  k_win_counts<<<grid_for(m, 256), 256, 0, s>>>(m, b_ncols, W.off, W.wins, W.nwin, cnt);
+  cudaMemsetAsync(cnt, 0, 2 * NBUCKET * sizeof(unsigned long long), s);
+  k_win_counts<<<grid_for(m, 256), 256, 0, s>>>(m, b_ncols, W.off, W.wins, W.nwin, span_hi, out_off, cnt);
   if (int rc = check_cuda("k_win_counts")) return rc;
-  unsigned long long h[NBUCKET];
+  unsigned long long h[2 * NBUCKET];
   cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric sync", 0);
-  int64_t nwork = 0;
-  unsigned long long cur[NBUCKET];
-  for (int i = 0; i < NBUCKET; ++i) {
-    cur[i] = (unsigned long long)nwork;
-    nwork += (int64_t)h[i];
+  int64_t nwork = 0, nsmall = 0;
+  unsigned long long cur[2 * NBUCKET];
+  for (int c : {1, 0}) {
+    for (int i = 0; i < NBUCKET; ++i) {
+      cur[c * NBUCKET + i] = (unsigned long long)nwork;
+      nwork += (int64_t)h[c * NBUCKET + i];
+    }
+    if (c == 1) nsmall = nwork;
   }
   if (nwork == 0) return SG_OK;
   if (nwork > work_cap) {
@@ -2079,26 +2117,28 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
     ktimer_end(s);
     if (int rc = check_cuda("k_expand")) return rc;
   }
-  // the ticket lives after the bucket cursors (host copy above must finish first)
-  unsigned long long* ticket = cnt + NBUCKET;
-  cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), s);
-  constexpr size_t sm = bmr_smem();
+  // tickets live after the cursors (the host copy above must finish first)
+  unsigned long long* tickets = cnt + 2 * NBUCKET;
+  cudaMemsetAsync(tickets, 0, 2 * sizeof(unsigned long long), s);
   const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
   const BTile bt{W.btile_off, W.btile};
-  const int grid = (int)std::min<int64_t>(nwork, (int64_t)num_sms() * WIN_CTAS);
   ktimer_begin("k_bmr", s);
-  if (dtype == SG_F64) {
-    auto kern = k_bmr<double>;
-    if (int rc = set_smem(kern, sm)) return rc;
-    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, bt, W.bm_save, W.pre_save, out_col, (double*)out_val,
-                                  ticket);
-  } else {
-    auto kern = k_bmr<float>;
-    if (int rc = set_smem(kern, sm)) return rc;
-    kern<<<grid, WIN_NT, sm, s>>>(nwork, work, A, B, bt, W.bm_save, W.pre_save, out_col, (float*)out_val, ticket);
+  if (nsmall > 0) {
+    int rc = dtype == SG_F64
+                 ? launch_bmr<double, SMALL_NT, SMALL_WORDS, SMALL_R, 2>(nsmall, work, A, B, bt, W, out_col, out_val,
+                                                                           tickets, s)
+                 : launch_bmr<float, SMALL_NT, SMALL_WORDS, SMALL_R, 2>(nsmall, work, A, B, bt, W, out_col, out_val,
+                                                                          tickets, s);
+    if (rc) return rc;
+  }
+  if (nwork > nsmall) {
+    int rc = dtype == SG_F64 ? launch_bmr<double, WIN_NT, WIN_WORDS, WIN_R, 1>(nwork - nsmall, work + nsmall, A, B,
+                                                                                bt, W, out_col, out_val, tickets + 1, s)
+                             : launch_bmr<float, WIN_NT, WIN_WORDS, WIN_R, 1>(nwork - nsmall, work + nsmall, A, B, bt,
+                                                                               W, out_col, out_val, tickets + 1, s);
+    if (rc) return rc;
   }
   ktimer_end(s);
-  if (int rc = check_cuda("k_bmr")) return rc;
   // `cur` (host) is read by the async copy above: keep it alive until done
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric end", 0);
   return SG_OK;

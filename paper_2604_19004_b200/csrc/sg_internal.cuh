@@ -17,7 +17,7 @@ struct Workspace {
   int32_t* rowlist;     // int32[m]   rows grouped by bin
   int64_t* tmp;         // int64[m+1] flags / scan scratch
   int64_t* partials;    // int64[nb+2] scan block partials
-  int64_t* bincnt;      // int64[128] bin histogram + cursors + ticket
+  int64_t* bincnt;      // int64[256] bin histogram + cursors + tickets
   size_t bytes;
 };
 
@@ -30,7 +30,7 @@ inline size_t workspace_bytes(int64_t m) {
   b += align256(4 * (size_t)m);
   b += align256(8 * ((size_t)m + 1));
   b += align256(8 * ((size_t)scan_tiles(m + 1) + 2));
-  b += align256(8 * 128);
+  b += align256(8 * 256);
   return b + 256;
 }
 
