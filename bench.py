@@ -194,12 +194,15 @@ def kernel_times(lib):
     return out
 
 
-def ncu_traffic(config, kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu launch list."""
+def ncu_traffic(config, kernel, brackets_per_step=1):
+    """DRAM bytes of `kernel` per timed bracket, from the committed ncu launch
+    list of one step of the same command (a bracket may span several launches,
+    e.g. the two window-kernel classes)."""
     p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f)[config][kernel]["dram_bytes_per_launch"]
+            d = json.load(f)[config][kernel]
+        return d.get("dram_bytes_per_step", d["dram_bytes_per_launch"] * d["launches"]) / max(brackets_per_step, 1)
     except (OSError, KeyError, ValueError):
         return None
 
@@ -209,7 +212,7 @@ def ncu_dominant(config):
     try:
         with open(p) as f:
             d = json.load(f)[config]
-        return max(d, key=lambda k: d[k]["us_per_launch"] * d[k]["launches"])
+        return max(d, key=lambda k: d[k].get("us_per_step", d[k]["us_per_launch"] * d[k]["launches"]))
     except (OSError, KeyError, ValueError):
         return None
 
@@ -369,7 +372,7 @@ def main():
               + (vbytes if ws_["saved_bitmaps"] else 4 + vbytes) * ws_["nnz_c"])
         kms_, kn_ = ktimes[dk]
         ach = kb / (kms_ / kn_ * 1e-3) / 1e9
-        traffic = ncu_traffic(args.config, dk)
+        traffic = ncu_traffic(args.config, dk, kn_ / args.steps)
         roof = {"bound": "hbm", "kernel": dk, "achieved": ach, "peak": peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
                 "algorithmic_bytes_per_launch": kb, "ms_per_launch": kms_ / kn_,

@@ -35,7 +35,8 @@ if "--json" in sys.argv:
         f[0] += a["dram__bytes_read.sum"] + a["dram__bytes_write.sum"]
         f[1] += a["gpu__time_duration.sum"]
         f[2] += cnt[k]
-    print(json.dumps({k: {"dram_bytes_per_launch": v[0] / v[2], "us_per_launch": v[1] / v[2], "launches": v[2]}
+    print(json.dumps({k: {"dram_bytes_per_launch": v[0] / v[2], "us_per_launch": v[1] / v[2], "launches": v[2],
+                          "dram_bytes_per_step": v[0], "us_per_step": v[1]}
                       for k, v in fam.items()}, indent=1))
     sys.exit(0)
 tot_t = sum(a["gpu__time_duration.sum"] for a in agg.values())
