@@ -1172,7 +1172,14 @@ struct WinAddOp {
 #endif
     const uint2 p = lds_u2(wp + (x >> 5) * 8);
     const uint32_t r = p.y + __popc(p.x & ((2u << (x & 31)) - 1u)) - 1u;
+#if defined(SG_PASS2_MODE) && SG_PASS2_MODE == 3
+    // experiment: racy plain add (wrong values, timing only)
+    double o;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(o) : "r"(vals + r * 8));
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(vals + r * 8), "d"(o + v) : "memory");
+#else
     smem_add_f64(vals + r * 8, v);
+#endif
   }
 };
 
