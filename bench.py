@@ -262,9 +262,17 @@ def main():
     from paper_2604_19004_b200 import EngineConfig, _lib, spgemm
     from paper_2604_19004_b200.device import DeviceCsr, to_device
 
+    # test hooks for the N>1 path on a one-GPU box: every rank on cuda:0 over gloo
+    same_dev = os.environ.get("SG_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     lib = _lib.load()

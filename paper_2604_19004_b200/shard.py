@@ -100,7 +100,7 @@ def _as_tensor(x, dtype, device):
     return torch.from_numpy(np.ascontiguousarray(x)).to(device=device, dtype=dtype)
 
 
-def row_products(a_ptr: torch.Tensor, a_col: torch.Tensor, b_ptr: torch.Tensor) -> np.ndarray:
+def row_products(a_ptr: torch.Tensor, a_col: torch.Tensor, b_ptr: torch.Tensor, b_col=None, b_ncols=None) -> np.ndarray:
     """Products per row of A (analysis.py:100-104) for partitioning, as a
     gather + cumsum over torch tensors (used on CPU test ranks; the GPU path
     uses the row-stats kernel)."""
@@ -131,7 +131,7 @@ def spgemm_sharded(a, b, local_fn, group=None, root=0, device=None, gather=False
     # balanced cuts computed on the root and broadcast
     cuts_t = torch.empty(world + 1, dtype=torch.int64, device=device)
     if rank == root:
-        per = (products_fn or row_products)(A[2], A[3], B[2])
+        per = (products_fn or row_products)(A[2], A[3], B[2], B[3], B[1])
         cuts_t.copy_(torch.tensor(balanced_cuts(per, world), dtype=torch.int64))
     dist.broadcast(cuts_t, src=root, group=group)
     cuts = [int(x) for x in cuts_t.tolist()]
@@ -152,14 +152,30 @@ def spgemm_sharded(a, b, local_fn, group=None, root=0, device=None, gather=False
 
 
 def gather_shards(shard: Shard, counts, cuts, root, group, device):
-    """Stitch the shards into one CSR on `root` (NCCL/gloo point-to-point)."""
+    """Stitch the shards into one CSR on `root` (NCCL/gloo point-to-point).
+    gloo has no device point-to-point, so with gloo device shards travel
+    through host copies."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    device = torch.device(device)
+    via_host = device.type == "cuda" and dist.get_backend(group) == "gloo"
+
+    def send(t, dst):
+        dist.send(t.cpu() if via_host else t, dst=dst, group=group)
+
+    def recv_into(t, src):
+        if via_host:
+            h = torch.empty(t.shape, dtype=t.dtype)
+            dist.recv(h, src=src, group=group)
+            t.copy_(h)
+        else:
+            dist.recv(t, src=src, group=group)
+
     if rank != root:
         if shard.col_idx.numel():
-            dist.send(shard.col_idx, dst=root, group=group)
-            dist.send(shard.values, dst=root, group=group)
-        dist.send(shard.row_ptr, dst=root, group=group)
+            send(shard.col_idx, root)
+            send(shard.values, root)
+        send(shard.row_ptr, root)
         return shard
     nrows = cuts[-1]
     total = int(sum(counts))
@@ -176,10 +192,10 @@ def gather_shards(shard: Shard, counts, cuts, root, group, device):
             rp = shard.row_ptr
         else:
             if n:
-                dist.recv(col[off:off + n], src=r, group=group)
-                dist.recv(val[off:off + n], src=r, group=group)
+                recv_into(col[off:off + n], r)
+                recv_into(val[off:off + n], r)
             rp = torch.empty(hi - lo + 1, dtype=torch.int64, device=device)
-            dist.recv(rp, src=r, group=group)
+            recv_into(rp, r)
         row_ptr[lo:hi + 1] = rp + off
         off += n
     return Shard(0, nrows, 0, total, row_ptr, col, val, shard.report)
@@ -190,12 +206,11 @@ def gpu_products_fn(device):
     from .device import DeviceCsr
     from .engine import _Ctx, row_stats
 
-    def fn(a_ptr, a_col, b_ptr):
+    def fn(a_ptr, a_col, b_ptr, b_col, b_ncols):
         ctx = _Ctx(device, torch.cuda.current_stream(device))
         m = a_ptr.numel() - 1
         A = DeviceCsr(m, b_ptr.numel() - 1, a_ptr, a_col, torch.empty(0, device=device))
-        B = DeviceCsr(b_ptr.numel() - 1, 0, b_ptr, torch.empty(0, dtype=torch.int32, device=device),
-                      torch.empty(0, device=device))
+        B = DeviceCsr(b_ptr.numel() - 1, int(b_ncols), b_ptr, b_col, torch.empty(0, device=device))
         prod, _, _, _ = row_stats(ctx, A, B)
         return prod.cpu().numpy()
     return fn
