@@ -335,28 +335,37 @@ __device__ __forceinline__ void bitonic_kv(int* keys, double* vals, int n, int g
 
 template <int IPT>
 __device__ __forceinline__ void warp_bitonic_reg(uint32_t (&r)[IPT], int lane) {
+  // Direction of stage k for element e = lane * IPT + i is ((e & k) == 0):
+  // for k < IPT it depends on i only (compile-time), for k >= IPT on the
+  // lane only (one test per stage), so no per-element index math remains.
 #pragma unroll
   for (int k = 2; k <= 32 * IPT; k <<= 1) {
+    const bool asc_lane = ((lane * IPT) & k) == 0;
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
       if (j >= IPT) {
         const int lm = j / IPT;
-        const bool lower = (lane & lm) == 0;
+        const bool keep_min = ((lane & lm) == 0) == asc_lane;
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
-          const bool asc = ((lane * IPT + i) & k) == 0;
           const uint32_t o = __shfl_xor_sync(SG_FULL, r[i], lm);
-          r[i] = (lower == asc) ? min(r[i], o) : max(r[i], o);
+          r[i] = keep_min ? min(r[i], o) : max(r[i], o);
         }
       } else {
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
           const int p = i ^ j;
           if (p > i) {
-            const bool asc = ((lane * IPT + i) & k) == 0;
             const uint32_t a = r[i], b = r[p];
-            r[i] = asc ? min(a, b) : max(a, b);
-            r[p] = asc ? max(a, b) : min(a, b);
+            const uint32_t lo = min(a, b), hi = max(a, b);
+            if (k < IPT) {
+              const bool asc = (i & k) == 0;  // compile-time
+              r[i] = asc ? lo : hi;
+              r[p] = asc ? hi : lo;
+            } else {
+              r[i] = asc_lane ? lo : hi;
+              r[p] = asc_lane ? hi : lo;
+            }
           }
         }
       }
