@@ -1709,12 +1709,14 @@ __global__ void k_classify_numeric(int64_t m, const int8_t* __restrict__ kind, c
                                    const int64_t* __restrict__ alloc, const int64_t* __restrict__ products,
                                    const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
                                    uint8_t* __restrict__ bins, int64_t* __restrict__ counts,
-                                   uint8_t* __restrict__ overflow, const int32_t* __restrict__ nwin) {
+                                   uint8_t* __restrict__ overflow, const int32_t* __restrict__ nwin,
+                                   const int64_t* __restrict__ exact) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int64_t p = products[i];
   const int8_t k = kind[i];
   uint8_t b;
+  const int64_t ex = exact ? exact[i] : -1;
   // rows with numeric windows (exact counts known) go to the window kernel
   if (p == 0 || k == SG_KIND_FALLBACK || (nwin && nwin[i] > 0)) {
     b = BIN_NONE;
@@ -1727,8 +1729,14 @@ __global__ void k_classify_numeric(int64_t m, const int8_t* __restrict__ kind, c
       b = BIN_ESC;
     } else if (k == SG_KIND_DENSE) {
       b = bm_bin(span);
+    } else if (ex >= 0 && limit != NOLIMIT && ex > limit) {
+      // known overflow (exact count over the tier limit): rerun in fallback
+      b = BIN_NONE;
+      counts[i] = 0;
+      overflow[i] = 1;
     } else {
-      const int64_t need = min(limit == NOLIMIT ? p : limit + 1, p);
+      // with an exact count the table holds exactly those keys
+      const int64_t need = ex >= 0 ? max(ex, (int64_t)1) : min(limit == NOLIMIT ? p : limit + 1, p);
       const int64_t T = max(pow2_at_least(2 * need), (int64_t)32);
       if (T <= 1024 && p <= 4096)
         b = (uint8_t)(BIN_HW0 + log2_pow2(T) - 5);
@@ -2005,15 +2013,15 @@ int sg_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, cons
                const void* a_val, const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
                const int8_t* kind, const int64_t* cap, const int64_t* alloc, const int64_t* products,
                const int64_t* span_lo, const int64_t* span_hi, const int64_t* out_off, int32_t* out_col,
-               void* out_val, int64_t* counts, uint8_t* overflow, const int32_t* skip_nwin, void* ws,
-               size_t ws_bytes, void* stream) {
+               void* out_val, int64_t* counts, uint8_t* overflow, const int32_t* skip_nwin,
+               const int64_t* exact, void* ws, size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   if (m == 0) return SG_OK;
   (void)b_ncols;
   cudaStream_t s = (cudaStream_t)stream;
   k_classify_numeric<<<grid_for(m, 256), 256, 0, s>>>(m, kind, cap, alloc, products, span_lo, span_hi, w.bins,
-                                                      counts, overflow, skip_nwin);
+                                                      counts, overflow, skip_nwin, exact);
   if (int rc = check_cuda("k_classify_numeric")) return rc;
   Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, kind, cap, alloc, span_lo, span_hi,
            out_off, out_col, out_val, counts, overflow, s};

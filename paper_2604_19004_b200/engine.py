@@ -411,7 +411,8 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     if m:
         _lib.call("sg_numeric", m, n, dcode, *Aargs, ptr(kind), ptr(cap), ptr(alloc),
                   ptr(products), ptr(span_lo), ptr(span_hi), ptr(out_off), ptr(out_col), ptr(out_val),
-                  ptr(counts), ptr(overflow), ptr(win.nwin) if win else None, ws, wsb, ctx.sp)
+                  ptr(counts), ptr(overflow), ptr(win.nwin) if win else None, ptr(pred) if exact else None,
+                  ws, wsb, ctx.sp)
     ev[4].record(ctx.stream)
     ctx.sync()
     t4 = time.perf_counter()
