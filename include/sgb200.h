@@ -153,11 +153,14 @@ int sg_window_capacity(int64_t m, const int64_t* products, const int64_t* span_l
  * binning: hash-counted rows are sized by
  * products / assist_cr (the conservative sampled CR, predict.py:111-118)
  * and rows whose table fills are recounted with product sizing; 1 = the
- * reference's product sizing.  Counts are exact either way. */
+ * reference's product sizing.  Counts are exact either way.  Rows with
+ * 0 < products <= min(skip_max_products, 1024) are not counted (counts = -2):
+ * the caller accumulates them into a staging slab instead (0 = count all). */
 int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col,
                 const int64_t* b_ptr, const int32_t* b_col, const int64_t* products,
                 const int64_t* span_lo, const int64_t* span_hi, int64_t* counts,
-                const sg_windows_t* win, double assist_cr, void* ws, size_t ws_bytes, void* stream);
+                const sg_windows_t* win, double assist_cr, int64_t skip_max_products, void* ws,
+                size_t ws_bytes, void* stream);
 
 /* Long-row numeric pass over the recorded windows: one CTA (1024 threads)
  * per window, work grouped by column range so concurrent CTAs share B-row

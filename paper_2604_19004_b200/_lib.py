@@ -52,7 +52,7 @@ SIGNATURES = {
     "sg_hll_build": (I32, [I64, P, P, I32, P, P]),
     "sg_hll_estimate": (I32, [I64, P, P, P, P, I32, P, D, P, P]),
     "sg_window_capacity": (I32, [I64, P, P, P, P, P, P, P, P, SZ, P]),
-    "sg_symbolic": (I32, [I64, I64, P, P, P, P, P, P, P, P, C.POINTER(SgWindows), D, P, SZ, P]),
+    "sg_symbolic": (I32, [I64, I64, P, P, P, P, P, P, P, P, C.POINTER(SgWindows), D, I64, P, SZ, P]),
     "sg_window_numeric": (I32, [I64, I64, I32, P, P, P, P, P, P, P, P, C.POINTER(SgWindows), P, P, P, P,
                                 I64, P, SZ, P]),
     "sg_btile_plan": (I32, [I64, I64, P, I64, P, P, P, SZ, P]),

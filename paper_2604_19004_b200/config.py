@@ -116,6 +116,9 @@ class EngineConfig:
     # size hash-counted rows of the symbolic pass by products / conservative
     # CR; counts stay exact (overfull rows are recounted)
     assisted_symbolic: bool = True
+    # symbolic workflow: rows of <= 1024 products skip the count pass and are
+    # accumulated once into a product-sized staging slab, then compacted
+    stage_short_rows: bool = True
 
     def __post_init__(self):
         if self.registers is not None and self.registers not in PRECISION_FOR:

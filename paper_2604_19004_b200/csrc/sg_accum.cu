@@ -1671,13 +1671,16 @@ __device__ __forceinline__ int64_t pow2_at_least(int64_t x) {
 // kernel and recounted with product sizing (rerun = 1 classifies only those).
 __global__ void k_classify_count(int64_t m, const int64_t* __restrict__ products, const int64_t* __restrict__ lo,
                                  const int64_t* __restrict__ hi, uint8_t* __restrict__ bins,
-                                 int64_t* __restrict__ counts, double crc, int rerun) {
+                                 int64_t* __restrict__ counts, double crc, int rerun, int64_t skip_max) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int64_t p = products[i];
   uint8_t b;
-  if (rerun && counts[i] >= 0) {
+  if (rerun && counts[i] != -1) {
     b = BIN_NONE;
+  } else if (!rerun && p > 0 && p <= skip_max && p <= 1024) {
+    b = BIN_NONE;  // short row left to a staged numeric pass: -2 = not counted
+    counts[i] = -2;
   } else if (p == 0) {
     b = BIN_NONE;
     counts[i] = 0;
@@ -1699,7 +1702,7 @@ __global__ void k_classify_count(int64_t m, const int64_t* __restrict__ products
 __global__ void k_count_negative(int64_t m, const int64_t* __restrict__ counts, unsigned long long* __restrict__ n) {
   int c = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-    c += counts[i] < 0;
+    c += counts[i] == -1;
   c = __reduce_add_sync(SG_FULL, c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(n, (unsigned long long)c);
 }
@@ -1979,14 +1982,15 @@ static Win to_win(const sg_windows_t* w) {
 
 int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t* a_col, const int64_t* b_ptr,
                 const int32_t* b_col, const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
-                int64_t* counts, const sg_windows_t* win, double assist_cr, void* ws, size_t ws_bytes,
-                void* stream) {
+                int64_t* counts, const sg_windows_t* win, double assist_cr, int64_t skip_max_products, void* ws,
+                size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   if (m == 0) return SG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const double crc = assist_cr > 1.0 ? assist_cr : 1.0;
-  k_classify_count<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, w.bins, counts, crc, 0);
+  k_classify_count<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, w.bins, counts, crc, 0,
+                                                    skip_max_products);
   if (int rc = check_cuda("k_classify_count")) return rc;
   Launch L{{a_ptr, a_col, nullptr}, {b_ptr, b_col, nullptr}, nullptr, nullptr, nullptr, span_lo, span_hi,
            nullptr, nullptr, nullptr, counts, nullptr, s};
@@ -2003,7 +2007,7 @@ int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t*
   cudaMemcpyAsync(&h, nneg, sizeof(h), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_symbolic sync", 0);
   if (h == 0) return SG_OK;
-  k_classify_count<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, w.bins, counts, 1.0, 1);
+  k_classify_count<<<grid_for(m, 256), 256, 0, s>>>(m, products, span_lo, span_hi, w.bins, counts, 1.0, 1, 0);
   if (int rc = check_cuda("k_classify_count")) return rc;
   L.win = Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // bitmap rows are done
   return run_bins<0, double>(L, m, w, nullptr);

@@ -190,6 +190,10 @@ class Windows:
         self.pre_save = None
 
 
+# symbolic workflow: rows with at most this many products are staged, not counted
+SHORT_ROW_PRODUCTS = 1024
+SHORT_ROW_MAX_CR = 1.25
+
 # saved key bitmaps may use at most this share of the free device memory
 BITMAP_SAVE_SHARE = 0.35
 
@@ -355,15 +359,30 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     # ---- size prediction (predict.py)
     ws, wsb = ctx.workspace(max(m, 1))
     win = None
+    short = None       # symbolic: rows staged instead of counted
+    pred_plan = None
     if kind_wf is WorkflowKind.SYMBOLIC:
         pred = ctx.empty(m, torch.int64)
         win = windows(ctx, m, products, span_lo, span_hi, None)
         # assisted symbolic binning with the conservative
         # sampled CR (predict.py:111-118) when the sample was taken
         assist = 1.0 if (cr is None or not cfg.assisted_symbolic) else max(1.0, cr[1] - 2.0 * cr[2])
+        # short rows (<= 1024 products) skip the count pass and are accumulated
+        # once into a staging slab sized by their products (the reference's
+        # staging rule is checked on exact counts, so not with a staging limit)
+        # -- only when the sampled compression ratio says products ~ outputs
+        # (otherwise the product-sized tables cost more than the count pass)
+        short_max = SHORT_ROW_PRODUCTS if (cfg.stage_short_rows and cfg.staging_limit_bytes is None
+                                           and cr is not None and cr[1] <= SHORT_ROW_MAX_CR) else 0
         _lib.call("sg_symbolic", m, n, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
-                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(pred), win.struct(), assist, ws, wsb, ctx.sp)
+                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(pred), win.struct(), assist, short_max,
+                  ws, wsb, ctx.sp)
         pred_kind = "exact"
+        if short_max and m:
+            staged = pred == -2
+            if bool(staged.any()):
+                short = staged
+                pred_plan = torch.where(short, products, pred)
     elif kind_wf is WorkflowKind.HLL_ESTIMATION:
         pred = hll_estimate(ctx, A, regs, p)
         pred_kind = "estimated"
@@ -385,7 +404,9 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     cap = ctx.empty(m, torch.int64)
     alloc = ctx.empty(m, torch.int64)
     ts = tiers_struct(tiers)
-    _lib.call("sg_plan", m, _PRED_CODE[pred_kind], ptr(pred), ptr(products), ptr(span_lo), ptr(span_hi),
+    if pred_plan is None:
+        pred_plan = pred
+    _lib.call("sg_plan", m, _PRED_CODE[pred_kind], ptr(pred_plan), ptr(products), ptr(span_lo), ptr(span_hi),
               ts, ptr(kind), ptr(cap), ptr(alloc), ctx.sp)
     staging_bytes = int(alloc.sum().item()) * 12 if m else 0  # engine.py:259 rule
     if cfg.staging_limit_bytes is not None and staging_bytes > cfg.staging_limit_bytes:
@@ -397,6 +418,20 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     exact = pred_kind == "exact"
     dcode = _dtype_code(A.values)
     Aargs = (ptr(A.row_ptr), ptr(A.col_idx), ptr(A.values), ptr(B.row_ptr), ptr(B.col_idx), ptr(B.values))
+    st_off = st_col = st_val = counts_s = None
+    if exact and short is not None:
+        # short rows: one numeric pass into a slab at their product offsets;
+        # their counts complete the exact row sizes
+        st_off = scan(ctx, torch.where(short, alloc, torch.zeros_like(alloc)))
+        st_total = int(st_off[-1].item())
+        st_col, st_val = ctx.empty(st_total, torch.int32), ctx.empty(st_total, dtype)
+        counts_s = ctx.empty(m, torch.int64)
+        _lib.call("sg_numeric", m, n, dcode, *Aargs, ptr(kind), ptr(cap), ptr(alloc),
+                  ptr(products), ptr(span_lo), ptr(span_hi), ptr(st_off), ptr(st_col), ptr(st_val),
+                  ptr(counts_s), ptr(overflow), ptr((~short).to(torch.int32)), None, ws, wsb, ctx.sp)
+        if bool(overflow[short].any()):  # cannot happen: slots hold every product
+            raise RuntimeError("internal: a staged short row overflowed its product-sized slot")
+        pred = torch.where(short, counts_s, pred)
     if exact:
         row_ptr = scan(ctx, pred)
         nnz_c = int(row_ptr[-1].item()) if m else 0
@@ -409,10 +444,16 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         out_col = ctx.empty(slab, torch.int32)
         out_val = ctx.empty(slab, dtype)
     if m:
+        skip = win.nwin if win else None
+        ovf = overflow
+        if short is not None:
+            skip = ((win.nwin[:m] > 0) | short).to(torch.int32)
+            ovf = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
         _lib.call("sg_numeric", m, n, dcode, *Aargs, ptr(kind), ptr(cap), ptr(alloc),
                   ptr(products), ptr(span_lo), ptr(span_hi), ptr(out_off), ptr(out_col), ptr(out_val),
-                  ptr(counts), ptr(overflow), ptr(win.nwin) if win else None, ptr(pred) if exact else None,
-                  ws, wsb, ctx.sp)
+                  ptr(counts), ptr(ovf), ptr(skip), ptr(pred) if exact else None, ws, wsb, ctx.sp)
+        if short is not None:
+            overflow |= ovf
     ev[4].record(ctx.stream)
     ctx.sync()
     t4 = time.perf_counter()
@@ -459,6 +500,10 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     _check_deadline(deadline)
 
     # ---- post-processing: hash rows were sorted in-kernel; compact the slab
+    if exact and short is not None:
+        _lib.call("sg_compact", m, _dtype_code(A.values), ptr(counts_s), ptr((~short).to(torch.uint8)),
+                  ptr(st_off), ptr(row_ptr), ptr(st_col), ptr(st_val), ptr(C_col), ptr(C_val), ctx.sp)
+        del st_col, st_val
     if not exact and m:
         skip = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
         if n_fb:

@@ -82,7 +82,7 @@ def test_stage_kernels_match_reference(gpu, name):
     ws, wsb = ctx.workspace(m)
     exact = torch.empty(m, dtype=torch.int64, device=gpu)
     L.call("sg_symbolic", m, B.ncols, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
-           ptr(products), ptr(lo), ptr(hi), ptr(exact), None, 1.0, ws, wsb, ctx.sp)
+           ptr(products), ptr(lo), ptr(hi), ptr(exact), None, 1.0, 0, ws, wsb, ctx.sp)
     np.testing.assert_array_equal(exact.cpu().numpy(), c.d["exact"])
     t = c.tiers() or TierConfig()
     est6 = hll_estimate(ctx, A, hll_build(ctx, B, 6), 6)
@@ -273,5 +273,5 @@ def test_assisted_symbolic_counts_exact(gpu, assist):
         ws, wsb = ctx.workspace(m)
         exact = torch.empty(m, dtype=torch.int64, device=gpu)
         L.call("sg_symbolic", m, B.ncols, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
-               ptr(products), ptr(lo), ptr(hi), ptr(exact), None, assist, ws, wsb, ctx.sp)
+               ptr(products), ptr(lo), ptr(hi), ptr(exact), None, assist, 0, ws, wsb, ctx.sp)
         np.testing.assert_array_equal(exact.cpu().numpy(), c.d["exact"], err_msg=name)
