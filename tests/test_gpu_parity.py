@@ -275,3 +275,29 @@ def test_assisted_symbolic_counts_exact(gpu, assist):
         L.call("sg_symbolic", m, B.ncols, ptr(A.row_ptr), ptr(A.col_idx), ptr(B.row_ptr), ptr(B.col_idx),
                ptr(products), ptr(lo), ptr(hi), ptr(exact), None, assist, 0, ws, wsb, ctx.sp)
         np.testing.assert_array_equal(exact.cpu().numpy(), c.d["exact"], err_msg=name)
+
+
+@pytest.mark.parametrize("force", [False, True])
+def test_staged_short_rows(gpu, monkeypatch, force):
+    """Symbolic workflow with short rows staged instead of counted (low-CR
+    gate; `force` lifts the gate so a high-CR matrix takes the path too)."""
+    from paper_2604_19004_b200 import EngineConfig, engine, matgen, spgemm
+    from oracle import ocean_cpu as oc
+    if force:
+        monkeypatch.setattr(engine, "SHORT_ROW_MAX_CR", 1e9)
+        a, b = matgen.poisson27(12), None
+    else:
+        rng = np.random.default_rng(7)
+        a = oc.triplets_to_csr(3000, 2000, np.repeat(np.arange(3000), 16), rng.integers(0, 2000, 48000),
+                               rng.uniform(0.5, 1.5, 48000))
+        b = oc.triplets_to_csr(2000, 900_000, np.repeat(np.arange(2000), 16), rng.integers(0, 900_000, 32000),
+                               rng.uniform(0.5, 1.5, 32000))
+    b = a if b is None else b
+    ref, rrep = oc.spgemm(a, b)
+    C, rep = spgemm(a, b, EngineConfig())
+    assert rep.workflow == rrep["workflow"] == "symbolic"
+    assert rep.kernel_ms["compact"] >= 0.0
+    np.testing.assert_array_equal(C.row_ptr, ref.row_ptr)
+    np.testing.assert_array_equal(C.col_idx, ref.col_idx)
+    np.testing.assert_allclose(C.values, ref.values, rtol=1e-12, atol=0)
+    assert rep.overflow_row_count == rrep["overflow_row_count"]
