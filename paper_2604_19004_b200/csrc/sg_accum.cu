@@ -100,16 +100,8 @@ __device__ __forceinline__ void plan_load(const Entries& E, int nent, int64_t p0
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       const bool ok = 32 * u < nvalid;
-#if defined(SG_PASS2_MODE) && SG_PASS2_MODE == 5
-      // experiment: operands from shared memory instead of L2 (wrong values)
-      extern __shared__ __align__(16) unsigned char smem[];
-      const int32_t* sc = reinterpret_cast<const int32_t*>(smem);
-      B.col[u] = ok ? sc[(lane + 32 * u) & 4095] + (int32_t)(base & 0) : 0;
-      B.v[u] = (VALUES && ok) ? a * 1.0 : 0.0;
-#else
       B.col[u] = ok ? __ldg(cp + 32 * u) : 0;
       B.v[u] = (VALUES && ok) ? a * (double)__ldg(vp + 32 * u) : 0.0;
-#endif
       B.valid |= ok ? (1u << u) : 0u;
     }
     if (seg_end == blk_end) ++c0;
@@ -877,21 +869,15 @@ __device__ __forceinline__ void emit_bits(unsigned long long bits, int32_t colba
 // the window accumulator): a window holds at most WIN_R distinct columns and
 // spans at most WIN_WORDS*64 columns, so its bitmap, rank prefix and values
 // all sit in shared memory.
-// SG_WIN_SPLIT = 2 halves the window (and the CTA) so two window CTAs share
-// an SM and overlap each other's latency-bound phases
-#ifndef SG_WIN_SPLIT
-#define SG_WIN_SPLIT 1
-#endif
-constexpr int WIN_CTAS = SG_WIN_SPLIT;           // window CTAs per SM
-constexpr int WIN_WORDS = 4096 / SG_WIN_SPLIT;   // 262,144 columns (split 1)
-constexpr int WIN_R = 16384 / SG_WIN_SPLIT;      // values per window (128 KB fp64, split 1)
+constexpr int WIN_WORDS = 4096;  // 262,144 columns
+constexpr int WIN_R = 16384;     // values per window (128 KB fp64)
 // Windows start on TILE_COLS-column tiles (absolute), so each selected B
 // row's segment in a window is two lookups in the B tile index (no search).
 constexpr int TILE_COLS = 4096;
 constexpr int TILE_WORDS = TILE_COLS / 64;
 constexpr int WIN_RP = WIN_R - TILE_COLS;  // a tile adds at most TILE_COLS keys
 constexpr int WIN_TILES = WIN_WORDS / TILE_WORDS;
-constexpr int WIN_NT = 1024 / SG_WIN_SPLIT;
+constexpr int WIN_NT = 1024;
 
 // bitmap origin of a windowed row: span_lo rounded down to a tile
 __host__ __device__ __forceinline__ int64_t win_origin(int64_t lo) { return lo & ~(int64_t)(TILE_COLS - 1); }
@@ -1090,43 +1076,6 @@ __device__ __forceinline__ int64_t lower_bound_col(const int32_t* __restrict__ c
   return s;
 }
 
-// Load a chunk of A entries whose B rows are clipped to columns [c0, c1).
-template <bool VALUES, typename V>
-__device__ __forceinline__ int64_t block_load_range(int64_t t, int64_t t1, int64_t c0, int64_t c1,
-                                                    const int32_t* __restrict__ a_col,
-                                                    const V* __restrict__ a_val,
-                                                    const int64_t* __restrict__ b_ptr,
-                                                    const int32_t* __restrict__ b_col, Entries E,
-                                                    int64_t* scr, int& nent) {
-  int64_t bs = 0, len = 0;
-  double av = 0.0;
-  if (t + threadIdx.x < t1) {
-    const int32_t k = a_col[t + threadIdx.x];
-    const int64_t s = b_ptr[k], e = b_ptr[k + 1];
-    if (e > s) {
-      const int64_t f = __ldg(b_col + s), l = __ldg(b_col + e - 1);
-      if (l >= c0 && f < c1) {
-        const int64_t ss = f >= c0 ? s : lower_bound_col(b_col, s, e, c0);
-        const int64_t ee = l < c1 ? e : lower_bound_col(b_col, ss, e, c1);
-        bs = ss;
-        len = ee - ss;
-      }
-    }
-    if (VALUES) av = (double)a_val[t + threadIdx.x];
-  }
-  // one scan of (len << 12 | nonempty): segment starts and compacted slots
-  int64_t tot;
-  const int64_t ex = block_excl_scan((len << 12) | (int64_t)(len > 0), scr, &tot);
-  const int64_t S = ex >> 12, pos = ex & 4095, P = tot >> 12, n64 = tot & 4095;
-  if (len > 0) {
-    E.S[pos] = S;
-    E.bs[pos] = bs;
-    if (VALUES) E.av[pos] = av;
-  }
-  __syncthreads();
-  nent = (int)n64;
-  return P;
-}
 
 template <bool VALUES, typename V, class Op>
 __device__ __forceinline__ void block_chunk_products(const Entries& E, int nent, int64_t P,
@@ -1230,18 +1179,6 @@ __device__ __forceinline__ void emit_bits32_smem(uint32_t bits, int32_t colbase,
   }
 }
 
-__device__ __forceinline__ void emit_bits_smem(unsigned long long bits, int32_t colbase, int* __restrict__ out) {
-  unsigned lo = (unsigned)bits, hi = (unsigned)(bits >> 32);
-  int k = 0;
-  while (lo) {
-    out[k++] = colbase + __ffs(lo) - 1;
-    lo &= lo - 1;
-  }
-  while (hi) {
-    out[k++] = colbase + 31 + __ffs(hi);
-    hi &= hi - 1;
-  }
-}
 
 #ifdef SG_PROF
 // phase cycle counters of the window kernel (profiling build only: make prof)
@@ -1256,26 +1193,6 @@ __device__ unsigned long long g_phase[12];
 #define SG_PH(i)
 #endif
 
-// position of the k-th (0-based) set bit of v
-__device__ __forceinline__ int nth_set_bit64(unsigned long long x, int k) {
-  unsigned v = (unsigned)x;
-  int pos = 0;
-  const int pl = __popc(v);
-  if (k >= pl) {
-    k -= pl;
-    v = (unsigned)(x >> 32);
-    pos = 32;
-  }
-  int p = __popc(v & 0xffffu);
-  if (k >= p) { k -= p; v >>= 16; pos += 16; }
-  p = __popc(v & 0xffu);
-  if (k >= p) { k -= p; v >>= 8; pos += 8; }
-  p = __popc(v & 0xfu);
-  if (k >= p) { k -= p; v >>= 4; pos += 4; }
-  p = __popc(v & 0x3u);
-  if (k >= p) { k -= p; v >>= 2; pos += 2; }
-  return pos + (k >= (int)(v & 1u) ? 1 : 0);
-}
 
 // One numeric window, resolved before launch: a CTA needs a single load.
 struct WinItem {
