@@ -1387,37 +1387,36 @@ __global__ void __launch_bounds__(NT, CTAS) k_bmr(int64_t nwork, const WinItem* 
 }
 
 // Column expansion of the long rows from the saved key bitmaps and word
-// ranks: C.col_idx[row_ptr[row] + rank .. ] for every set bit, ascending.
-// One block per row (rows without windows are skipped), four words per
-// thread per step with the loads issued first, per-lane bit loop straight to
-// global memory.  (Block-staged, warp-staged and warp-cooperative variants
-// all measured slower on R-MAT-20: 64-80 ms vs 59 ms.)
+// ranks: C.col_idx[row_ptr[row] + rank ..] for every set bit, ascending.
+// Blocks sweep the window work items (each <= WIN_WORDS words, so the work is
+// even; a block per row left the hub rows as the tail: 62 vs 59 ms), four
+// words per thread per step with the loads issued first, per-lane bit loop
+// straight to global memory.  (Block-staged, warp-staged, warp-cooperative and
+// load-balanced variants all measured slower.)
 constexpr int EXP_NT = 256;
 
-__global__ void __launch_bounds__(EXP_NT) k_expand(int64_t m, const int32_t* __restrict__ nwin,
-                                                   const int64_t* __restrict__ bm_off,
-                                                   const unsigned long long* __restrict__ bm_save,
-                                                   const int32_t* __restrict__ pre_save,
-                                                   const int64_t* __restrict__ span_lo,
-                                                   const int64_t* __restrict__ out_off,
-                                                   int32_t* __restrict__ out_col) {
-  for (int64_t r = blockIdx.x; r < m; r += gridDim.x) {
-    if (nwin[r] <= 0) continue;
-    const int64_t w0 = bm_off[r], nw = bm_off[r + 1] - w0;
-    const int32_t org = (int32_t)win_origin(span_lo[r]);
-    int32_t* out = out_col + out_off[r];
+__global__ void __launch_bounds__(EXP_NT) k_expand_items(int64_t nwork, const WinItem* __restrict__ work,
+                                                         const unsigned long long* __restrict__ bm_save,
+                                                         const int32_t* __restrict__ pre_save,
+                                                         int32_t* __restrict__ out_col) {
+  for (int64_t b = blockIdx.x; b < nwork; b += gridDim.x) {
+    const WinItem it = work[b];
+    if (it.bm_word < 0) continue;
+    const int64_t nw = ((int64_t)it.c1 - it.c0 + 63) >> 6;
+    const int32_t r0 = __ldg(pre_save + it.bm_word);
+    int32_t* out = out_col + it.out_base;
     for (int64_t i0 = threadIdx.x; i0 < nw; i0 += 4 * EXP_NT) {
       unsigned long long bits[4];
       int32_t pos[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t i = i0 + u * EXP_NT;
-        bits[u] = i < nw ? __ldcs(bm_save + w0 + i) : 0ull;
-        pos[u] = i < nw ? __ldcs(pre_save + w0 + i) : 0;
+        bits[u] = i < nw ? __ldcs(bm_save + it.bm_word + i) : 0ull;
+        pos[u] = i < nw ? __ldcs(pre_save + it.bm_word + i) - r0 : 0;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        emit_bits(bits[u], org + (int32_t)(64 * (i0 + u * EXP_NT)), out + pos[u]);
+        emit_bits(bits[u], it.c0 + (int32_t)(64 * (i0 + u * EXP_NT)), out + pos[u]);
     }
   }
 }
@@ -2057,8 +2056,8 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   if (int rc = check_cuda("k_win_scatter")) return rc;
   if (W.bm_save) {
     ktimer_begin("k_expand", s);
-    k_expand<<<(int)std::min<int64_t>(m, (int64_t)num_sms() * 16), EXP_NT, 0, s>>>(
-        m, W.nwin, W.bm_off, W.bm_save, W.pre_save, span_lo, out_off, out_col);
+    k_expand_items<<<(int)std::min<int64_t>(nwork, (int64_t)num_sms() * 8), EXP_NT, 0, s>>>(
+        nwork, work, W.bm_save, W.pre_save, out_col);
     ktimer_end(s);
     if (int rc = check_cuda("k_expand")) return rc;
   }
