@@ -1783,9 +1783,10 @@ static int launch_bin(int bin, const Launch& L, const int32_t* rows, int64_t n) 
     case BIN_HBN: return launch_hb<11, MODE, V, 256>(L, rows, n);
     case BIN_HB0 + 0: return launch_hb<12, MODE, V, 512>(L, rows, n);
     case BIN_HB0 + 1: return launch_hb<13, MODE, V, 512>(L, rows, n);
-    case BIN_HB0 + 2: return launch_hb<14, MODE, V, 512>(L, rows, n);
+    case BIN_HB0 + 2:  // numeric T = 16384 fills the SM's shared memory: one CTA with every thread
+      return MODE == 1 ? launch_hb<14, MODE, V, 1024>(L, rows, n) : launch_hb<14, MODE, V, 512>(L, rows, n);
     case BIN_HB0 + 3:
-      if (MODE == 0) return launch_hb<15, 0, V, 512>(L, rows, n);
+      if (MODE == 0) return launch_hb<15, 0, V, 1024>(L, rows, n);
       return SG_ERR_ARG;
     case BIN_BM0 + 0: return launch_bm<256, MODE, V, 256>(L, rows, n);
     case BIN_BM0 + 1: return launch_bm<2048, MODE, V, 256>(L, rows, n);
