@@ -319,7 +319,6 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     er = total_products / nnz_a if nnz_a else 0.0
     avg = total_products / m if m else 0.0
     ev[1].record(ctx.stream)
-    t1 = time.perf_counter()
     _check_deadline(deadline)
 
     # ---- sketch + sampled CR (engine.py:157-174)
@@ -352,8 +351,6 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         else:
             kind_wf = select_workflow(avg, er, cr[0])
     ev[2].record(ctx.stream)
-    ctx.sync()
-    t2 = time.perf_counter()
     _check_deadline(deadline)
 
     # ---- size prediction (predict.py)
@@ -390,8 +387,6 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         pred = products
         pred_kind = "upper_bound"
     ev[3].record(ctx.stream)
-    ctx.sync()
-    t3 = time.perf_counter()
     _check_deadline(deadline)
 
     # ---- binning (accumulate.plan_rows) + numeric phase (engine._numeric_phase)
@@ -408,7 +403,9 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         pred_plan = pred
     _lib.call("sg_plan", m, _PRED_CODE[pred_kind], ptr(pred_plan), ptr(products), ptr(span_lo), ptr(span_hi),
               ts, ptr(kind), ptr(cap), ptr(alloc), ctx.sp)
-    staging_bytes = int(alloc.sum().item()) * 12 if m else 0  # engine.py:259 rule
+    staging_bytes = 0
+    if cfg.staging_limit_bytes is not None and m:
+        staging_bytes = int(alloc.sum().item()) * 12  # engine.py:259 rule
     if cfg.staging_limit_bytes is not None and staging_bytes > cfg.staging_limit_bytes:
         raise ResourceLimitError(
             f"staged output needs {staging_bytes} bytes, over the {cfg.staging_limit_bytes} byte "
@@ -455,8 +452,6 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         if short is not None:
             overflow |= ovf
     ev[4].record(ctx.stream)
-    ctx.sync()
-    t4 = time.perf_counter()
     _check_deadline(deadline)
 
     # ---- fallback (engine._fallback_phase): overflow | planned FALLBACK rows
@@ -495,8 +490,6 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         _lib.call("sg_fallback", 1, n_rest, ptr(rest), n, dcode, *fargs, ptr(row_ptr),
                   ptr(C_col), ptr(C_val), ptr(counts), None, ws, wsb, ctx.sp)
     ev[5].record(ctx.stream)
-    ctx.sync()
-    t5 = time.perf_counter()
     _check_deadline(deadline)
 
     # ---- post-processing: hash rows were sorted in-kernel; compact the slab
@@ -516,7 +509,6 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         nnz_c = 0
     ev[6].record(ctx.stream)
     ctx.sync()
-    t6 = time.perf_counter()
     for i, name in enumerate(("analysis", "sketch", "predict", "numeric", "fallback", "compact")):
         kms[name] = ev[i].elapsed_time(ev[i + 1])
 
@@ -535,9 +527,11 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         workflow=kind_wf.value, registers=registers, er=er,
         cr_hat=None if cr is None else cr[0],
         cr_true=(total_products / nnz_c) if nnz_c else None,
-        analysis_ms=(t1 - t0) * 1e3, sketch_ms=(t2 - t1) * 1e3 if regs is not None else 0.0,
-        predict_ms=(t3 - t2) * 1e3, numeric_ms=(t4 - t3) * 1e3, fallback_ms=(t5 - t4) * 1e3,
-        compact_ms=(t6 - t5) * 1e3, total_ms=total_ms, overflow_row_count=n_fb, nnz_c=nnz_c,
+        # stage times from the CUDA events on the call's stream (the stages
+        # run back to back without host synchronisation in between)
+        analysis_ms=kms["analysis"], sketch_ms=kms["sketch"] if regs is not None else 0.0,
+        predict_ms=kms["predict"], numeric_ms=kms["numeric"], fallback_ms=kms["fallback"],
+        compact_ms=kms["compact"], total_ms=total_ms, overflow_row_count=n_fb, nnz_c=nnz_c,
         total_products=total_products, bitmap_query=bool(bitmap_query),
         est_mean_rel_err=est_mean, est_std_rel_err=est_std,
         gflops=(2.0 * total_products / (total_ms * 1e-3) / 1e9) if total_ms > 0 else None,
