@@ -22,6 +22,7 @@ Memory layout differences (results are identical):
 from __future__ import annotations
 
 import ctypes
+import threading
 import time
 from dataclasses import replace
 
@@ -102,6 +103,7 @@ class _Ctx:
         self.ws = None
         self.ws_bytes = 0
         self._old_ws = []
+        self.arena_taken = False
 
     def workspace(self, m):
         """Scratch for the stage calls.  A grown workspace never frees the
@@ -118,6 +120,13 @@ class _Ctx:
         try:
             return torch.empty(int(n), dtype=dtype, device=self.device)
         except torch.OutOfMemoryError as exc:
+            # buffers kept from earlier calls give way first
+            if _ARENA.drop_if_idle(self.device):
+                torch.cuda.empty_cache()
+                try:
+                    return torch.empty(int(n), dtype=dtype, device=self.device)
+                except torch.OutOfMemoryError:
+                    pass
             raise ResourceLimitError(
                 f"device allocation of {int(n)} x {dtype} failed; the symbolic workflow "
                 "(workflow='symbolic') stages exact-sized rows") from exc
@@ -210,16 +219,105 @@ def windows(ctx: _Ctx, m, products, lo, hi, select) -> Windows:
     nwin = torch.zeros(max(m, 1), dtype=torch.int32, device=ctx.device)
     bm_save = pre_save = None
     if total and words:
-        free, _ = torch.cuda.mem_get_info(ctx.device)
-        # blocks cached by torch's allocator are free for this purpose too
-        free += torch.cuda.memory_reserved(ctx.device) - torch.cuda.memory_allocated(ctx.device)
+        # free = device memory minus what torch has handed out (cached blocks
+        # and the arena's own buffers count as free); torch's counters, not
+        # cudaMemGetInfo, which costs milliseconds under expandable segments
+        free = _device_total(ctx.device) - torch.cuda.memory_allocated(ctx.device)
+        free += _ARENA.held_bytes(ctx.device)
         if 12 * words <= BITMAP_SAVE_SHARE * free:
-            try:
-                bm_save = torch.empty(words, dtype=torch.int64, device=ctx.device)
-                pre_save = torch.empty(words, dtype=torch.int32, device=ctx.device)
-            except torch.OutOfMemoryError:
-                bm_save = pre_save = None
+            got = _ARENA.take(ctx, words)
+            if got is not None:
+                bm_save, pre_save = got
     return Windows(off, wins, nwin, bm_off, bm_save, pre_save, total)
+
+
+_TOTAL: dict = {}
+
+
+def _device_total(device) -> int:
+    """Device memory usable by this process (total minus a 4 GB reserve for
+    the context and other processes), cached."""
+    key = str(device)
+    if key not in _TOTAL:
+        free, total = torch.cuda.mem_get_info(device)
+        _TOTAL[key] = max(0, min(total - (4 << 30), free + torch.cuda.memory_reserved(device)))
+    return _TOTAL[key]
+
+
+class _BitmapArena:
+    """Saved-bitmap buffers kept across calls, per device.  Allocating them
+    afresh (tens of GB at R-MAT-20) costs from 0.5 to 60 ms per call when the
+    caching allocator has to map new memory; reusing them removes that jitter.
+    A call holds the device's buffers until it returns; a concurrent call on
+    the same device allocates its own (and does not keep them)."""
+
+    HEADROOM = 1.02
+
+    def __init__(self):
+        self.lock = threading.Lock()
+        self.bufs: dict = {}
+        self.busy: set = set()
+
+    def held_bytes(self, device) -> int:
+        with self.lock:
+            b = self.bufs.get(str(device))
+        return 0 if b is None else b[0].numel() * 12
+
+    def take(self, ctx, words):
+        key = str(ctx.device)
+        with self.lock:
+            shared = key in self.busy
+            cur = None if shared else self.bufs.get(key)
+            if not shared:
+                self.busy.add(key)
+                if cur is not None and cur[0].numel() < words:
+                    del self.bufs[key]  # too small: replace
+                    cur = None
+        if cur is None:
+            n = words if shared else int(words * self.HEADROOM)
+            try:
+                cur = (torch.empty(n, dtype=torch.int64, device=ctx.device),
+                       torch.empty(n, dtype=torch.int32, device=ctx.device))
+            except torch.OutOfMemoryError:
+                try:
+                    cur = (torch.empty(words, dtype=torch.int64, device=ctx.device),
+                           torch.empty(words, dtype=torch.int32, device=ctx.device))
+                except torch.OutOfMemoryError:
+                    if not shared:
+                        self.release(ctx.device)
+                    return None
+            if not shared:
+                with self.lock:
+                    self.bufs[key] = cur
+        if not shared:
+            ctx.arena_taken = True
+        return cur[0][:words], cur[1][:words]
+
+    def release(self, device):
+        with self.lock:
+            self.busy.discard(str(device))
+
+    def drop(self, device):
+        """Free the device's buffers (C needs the memory)."""
+        with self.lock:
+            self.bufs.pop(str(device), None)
+
+    def drop_if_idle(self, device) -> bool:
+        with self.lock:
+            key = str(device)
+            if key in self.busy or key not in self.bufs:
+                return False
+            del self.bufs[key]
+            return True
+
+
+_ARENA = _BitmapArena()
+
+
+def release_bitmap_arena(device=None):
+    """Free the saved-bitmap buffers kept across calls."""
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    _ARENA.drop(dev)
 
 
 # the B tile index (sg_btile_plan) may use at most this many bytes
@@ -251,6 +349,7 @@ def alloc_c(ctx: _Ctx, nnz, dtype, win):
         if win is None or win.bm_save is None:
             raise
         win.drop_bitmaps()
+        _ARENA.drop(ctx.device)
         torch.cuda.empty_cache()
         return ctx.empty(nnz, torch.int32), ctx.empty(nnz, dtype)
 
@@ -291,7 +390,15 @@ def spgemm(a, b, cfg: EngineConfig | None = None, deadline: float | None = None)
     device = torch.device("cuda", cfg.device if cfg.device is not None else torch.cuda.current_device())
     stream = cfg.stream if cfg.stream is not None else torch.cuda.current_stream(device)
     with torch.cuda.device(device), torch.cuda.stream(stream):
-        return _spgemm(a, b, cfg, deadline, _Ctx(device, stream))
+        ctx = _Ctx(device, stream)
+        try:
+            return _spgemm(a, b, cfg, deadline, ctx)
+        finally:
+            if ctx.arena_taken:
+                # the call's work is complete (it ends with a stream sync on
+                # success); on an error, wait before the buffers are reused
+                ctx.sync()
+                _ARENA.release(device)
 
 
 def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
