@@ -195,14 +195,16 @@ int sg_scan(int64_t n, const int64_t* in, int64_t* out, void* ws, size_t ws_byte
  * sg_window_numeric.  exact (nullable): the rows' exact distinct counts
  * (symbolic workflow); hash tables are then sized by them instead of by the
  * tier capacity, and a row over its limit is flagged without accumulating
- * (same overflow set, same C). */
+ * (same overflow set, same C).  escr_max > 0: rows of <= min(escr_max, 512)
+ * products (columns < 2^23, not DENSE, within their limit) use the register
+ * expand-sort-compress accumulator (low-CR short rows; 0 = off). */
 int sg_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, const int32_t* a_col,
                const void* a_val, const int64_t* b_ptr, const int32_t* b_col, const void* b_val,
                const int8_t* kind, const int64_t* cap, const int64_t* alloc,
                const int64_t* products, const int64_t* span_lo, const int64_t* span_hi,
                const int64_t* out_off, int32_t* out_col, void* out_val, int64_t* counts,
-               uint8_t* overflow, const int32_t* skip_nwin, const int64_t* exact, void* ws, size_t ws_bytes,
-               void* stream);
+               uint8_t* overflow, const int32_t* skip_nwin, const int64_t* exact, int64_t escr_max,
+               void* ws, size_t ws_bytes, void* stream);
 
 /* Rows for the fallback pass (engine.py:202-203): overflow | (kind ==
  * FALLBACK & products > 0), ascending, minus rows with exclude_nwin[row] > 0

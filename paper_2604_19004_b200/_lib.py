@@ -59,7 +59,7 @@ SIGNATURES = {
     "sg_btile_build": (I32, [I64, I64, P, P, P, P, P, P]),
     "sg_plan": (I32, [I64, I32, P, P, P, P, C.POINTER(SgTiers), P, P, P, P]),
     "sg_scan": (I32, [I64, P, P, P, SZ, P]),
-    "sg_numeric": (I32, [I64, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]),
+    "sg_numeric": (I32, [I64, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, P, I64, P, SZ, P]),
     "sg_select_fallback": (I32, [I64, P, P, P, P, P, C.POINTER(C.c_int64), P, SZ, P]),
     "sg_fallback": (I32, [I32, I64, P, I64, I32, P, P, P, P, P, P, P, P, P, P, P, P, P,
                           C.POINTER(SgWindows), P, SZ, P]),

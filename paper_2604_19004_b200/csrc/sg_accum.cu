@@ -603,6 +603,113 @@ constexpr size_t hw_smem() {
 }
 
 // -------------------------------------------------------------------------
+// ESCR: warp-per-row register expand-sort-compress for short rows of low
+// compression ratio (products ~ outputs, e.g. the rect config): the products
+// are appended to a per-warp shared buffer, sorted as packed
+// (col << 9 | product slot) words in registers (warp_bitonic_reg), and
+// duplicate columns summed in slot order -- no hash table to clear, probe,
+// compact or sort.  Needs products <= 512 and columns < 2^23.
+
+constexpr int ESCR_WARPS = 4;
+constexpr int ESCR_MAX = 512;
+
+struct AppendOp {
+  int* keys;
+  double* vals;
+  int* n;
+  __device__ __forceinline__ void operator()(int32_t col, double v) {
+    const unsigned act = __activemask();
+    const int lane = lane_id();
+    const int leader = __ffs(act) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(n, __popc(act));
+    base = __shfl_sync(act, base, leader);
+    const int pos = base + __popc(act & lanemask_lt());
+    keys[pos] = col;
+    vals[pos] = v;
+  }
+};
+
+template <int IPT, typename V>
+__device__ __forceinline__ int escr_sort_reduce(int* keys, const double* vals, int n, int lane,
+                                                int32_t* __restrict__ oc, V* __restrict__ ov) {
+  uint32_t r[IPT];
+  uint32_t* pk = reinterpret_cast<uint32_t*>(keys);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int e = lane * IPT + i;
+    r[i] = e < n ? (((uint32_t)keys[e] << 9) | (uint32_t)e) : 0xFFFFFFFFu;
+  }
+  __syncwarp();
+  warp_bitonic_reg<IPT>(r, lane);
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int e = lane * IPT + i;
+    if (e < n) pk[e] = r[i];
+  }
+  __syncwarp();
+  // striped pass: a run head sums its run (slot order) and writes at the
+  // head's rank among heads
+  int out = 0;
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    const int e = e0 + lane;
+    const uint32_t k = e < n ? pk[e] : 0xFFFFFFFFu;
+    const bool head = e < n && (e == 0 || (pk[e - 1] >> 9) != (k >> 9));
+    const unsigned hb = __ballot_sync(SG_FULL, head);
+    if (head) {
+      double sum = vals[k & 511u];
+      for (int j = e + 1; j < n && (pk[j] >> 9) == (k >> 9); ++j) sum += vals[pk[j] & 511u];
+      const int pos = out + __popc(hb & lanemask_lt());
+      st_stream(oc + pos, (int32_t)(k >> 9));
+      st_stream(ov + pos, (V)sum);
+    }
+    out += __popc(hb);
+  }
+  return out;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(ESCR_WARPS * 32) k_escr(int64_t nbin, const int32_t* __restrict__ rows, Csr A,
+                                                          Csr B, const int64_t* __restrict__ out_off,
+                                                          int32_t* __restrict__ out_col, V* __restrict__ out_val,
+                                                          int64_t* __restrict__ counts,
+                                                          uint8_t* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int w = warp_id(), lane = lane_id();
+  constexpr size_t ENT = 3 * 33 * 8;
+  constexpr size_t PER = ENT + (size_t)ESCR_MAX * 12 + 16;
+  unsigned char* base = smem + (size_t)w * PER;
+  Entries E{reinterpret_cast<int64_t*>(base), reinterpret_cast<int64_t*>(base) + 33,
+            reinterpret_cast<double*>(base) + 66};
+  double* vals = reinterpret_cast<double*>(base + ENT);
+  int* keys = reinterpret_cast<int*>(base + ENT + (size_t)ESCR_MAX * 8);
+  int* n = keys + ESCR_MAX;
+  const int64_t wid = (int64_t)blockIdx.x * ESCR_WARPS + w;
+  if (wid >= nbin) return;
+  const int64_t row = rows[wid];
+  if (lane == 0) *n = 0;
+  __syncwarp();
+  AppendOp op{keys, vals, n};
+  warp_row<true, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, op, nullptr);
+  __syncwarp();
+  const int np = *n;
+  const int64_t off = out_off[row];
+  int cnt;
+  const int ipt = (np + 31) >> 5;
+  if (ipt <= 1) cnt = escr_sort_reduce<1, V>(keys, vals, np, lane, out_col + off, out_val + off);
+  else if (ipt <= 2) cnt = escr_sort_reduce<2, V>(keys, vals, np, lane, out_col + off, out_val + off);
+  else if (ipt <= 4) cnt = escr_sort_reduce<4, V>(keys, vals, np, lane, out_col + off, out_val + off);
+  else if (ipt <= 8) cnt = escr_sort_reduce<8, V>(keys, vals, np, lane, out_col + off, out_val + off);
+  else cnt = escr_sort_reduce<16, V>(keys, vals, np, lane, out_col + off, out_val + off);
+  if (lane == 0) {
+    counts[row] = cnt;
+    overflow[row] = 0;
+  }
+}
+
+constexpr size_t escr_smem() { return (size_t)ESCR_WARPS * (3 * 33 * 8 + (size_t)ESCR_MAX * 12 + 16); }
+
+// -------------------------------------------------------------------------
 // HB: block-per-row shared-memory hash
 
 template <int LOG2T, int MODE, typename V, int NT>
@@ -1564,7 +1671,8 @@ enum Bin : uint8_t {
   BIN_HB0 = 9,  // T = 4096 << (bin - BIN_HB0), up to 32768 (bins 9..12); numeric uses 2048..16384 via HB_N0
   BIN_BM0 = 13, // BW = 256, 2048, 16384 (bins 13..15)
   BIN_HBN = 16, // numeric HB T = 2048 (bin 16)
-  NBINS = 17
+  BIN_ESCR = 17, // numeric register expand-sort-compress, <= 512 products, low CR (bin 17)
+  NBINS = 18
 };
 
 __device__ __forceinline__ uint8_t bm_bin(int64_t span) {
@@ -1629,7 +1737,7 @@ __global__ void k_classify_numeric(int64_t m, const int8_t* __restrict__ kind, c
                                    const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
                                    uint8_t* __restrict__ bins, int64_t* __restrict__ counts,
                                    uint8_t* __restrict__ overflow, const int32_t* __restrict__ nwin,
-                                   const int64_t* __restrict__ exact) {
+                                   const int64_t* __restrict__ exact, int64_t escr_max) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int64_t p = products[i];
@@ -1646,6 +1754,8 @@ __global__ void k_classify_numeric(int64_t m, const int8_t* __restrict__ kind, c
     const int64_t limit = row_limit(kind, cap, alloc, i);
     if (k == SG_KIND_ESC && p <= 64) {
       b = BIN_ESC;
+    } else if (p <= escr_max && p <= ESCR_MAX && k != SG_KIND_DENSE && (limit == NOLIMIT || p <= limit)) {
+      b = BIN_ESCR;  // holds every product: cannot overflow while p <= limit
     } else if (k == SG_KIND_DENSE) {
       b = bm_bin(span);
     } else if (ex >= 0 && limit != NOLIMIT && ex > limit) {
@@ -1771,6 +1881,16 @@ static int launch_bin(int bin, const Launch& L, const int32_t* rows, int64_t n) 
         return check_cuda("k_esc");
       }
       return SG_ERR_ARG;
+    case BIN_ESCR:
+      if (MODE == 1) {
+        constexpr size_t sm = escr_smem();
+        auto kern = k_escr<V>;
+        if (int rc = set_smem(kern, sm)) return rc;
+        kern<<<grid_for(n, ESCR_WARPS), ESCR_WARPS * 32, sm, L.s>>>(n, rows, L.A, L.B, L.out_off, L.out_col,
+                                                                    (V*)L.out_val, L.counts, L.overflow);
+        return check_cuda("k_escr");
+      }
+      return SG_ERR_ARG;
     case BIN_HW0 + 0: return launch_hw<5, MODE, V>(L, rows, n);
     case BIN_HW0 + 1: return launch_hw<6, MODE, V>(L, rows, n);
     case BIN_HW0 + 2: return launch_hw<7, MODE, V>(L, rows, n);
@@ -1799,7 +1919,7 @@ static int launch_bin(int bin, const Launch& L, const int32_t* rows, int64_t n) 
 // bins in launch order: heaviest families first so they start early
 static const int kOrder[] = {BIN_BM0 + 2, BIN_HB0 + 3, BIN_HB0 + 2, BIN_HB0 + 1, BIN_HB0 + 0, BIN_BM0 + 1,
                              BIN_HBN,     BIN_BM0 + 0, BIN_HW0 + 6, BIN_HW0 + 5, BIN_HW0 + 4, BIN_HW0 + 3,
-                             BIN_HW0 + 2, BIN_HW0 + 1, BIN_HW0 + 0, BIN_ESC};
+                             BIN_HW0 + 2, BIN_HW0 + 1, BIN_HW0 + 0, BIN_ESC, BIN_ESCR};
 
 // Bins are independent: launch them on a few forked streams so the small
 // bins fill the tail of the big ones, then join back into the caller's stream.
@@ -1935,14 +2055,15 @@ int sg_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr, cons
                const int8_t* kind, const int64_t* cap, const int64_t* alloc, const int64_t* products,
                const int64_t* span_lo, const int64_t* span_hi, const int64_t* out_off, int32_t* out_col,
                void* out_val, int64_t* counts, uint8_t* overflow, const int32_t* skip_nwin,
-               const int64_t* exact, void* ws, size_t ws_bytes, void* stream) {
+               const int64_t* exact, int64_t escr_max, void* ws, size_t ws_bytes, void* stream) {
   Workspace w;
   if (!carve(ws, ws_bytes, m, w)) return SG_ERR_WORKSPACE;
   if (m == 0) return SG_OK;
   (void)b_ncols;
   cudaStream_t s = (cudaStream_t)stream;
   k_classify_numeric<<<grid_for(m, 256), 256, 0, s>>>(m, kind, cap, alloc, products, span_lo, span_hi, w.bins,
-                                                      counts, overflow, skip_nwin, exact);
+                                                      counts, overflow, skip_nwin, exact,
+                                                      b_ncols < ((int64_t)1 << 23) ? escr_max : 0);
   if (int rc = check_cuda("k_classify_numeric")) return rc;
   Launch L{{a_ptr, a_col, a_val}, {b_ptr, b_col, b_val}, kind, cap, alloc, span_lo, span_hi,
            out_off, out_col, out_val, counts, overflow, s};

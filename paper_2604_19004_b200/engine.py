@@ -202,6 +202,9 @@ class Windows:
 # symbolic workflow: rows with at most this many products are staged, not counted
 SHORT_ROW_PRODUCTS = 1024
 SHORT_ROW_MAX_CR = 1.25
+# staged short rows of at most this many products use the register
+# expand-sort-compress accumulator (0 = hash tables)
+SHORT_ROW_ESCR = 512
 
 # saved key bitmaps may use at most this share of the free device memory
 BITMAP_SAVE_SHARE = 0.35
@@ -532,7 +535,8 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         counts_s = ctx.empty(m, torch.int64)
         _lib.call("sg_numeric", m, n, dcode, *Aargs, ptr(kind), ptr(cap), ptr(alloc),
                   ptr(products), ptr(span_lo), ptr(span_hi), ptr(st_off), ptr(st_col), ptr(st_val),
-                  ptr(counts_s), ptr(overflow), ptr((~short).to(torch.int32)), None, ws, wsb, ctx.sp)
+                  ptr(counts_s), ptr(overflow), ptr((~short).to(torch.int32)), None, SHORT_ROW_ESCR,
+                  ws, wsb, ctx.sp)
         if bool(overflow[short].any()):  # cannot happen: slots hold every product
             raise RuntimeError("internal: a staged short row overflowed its product-sized slot")
         pred = torch.where(short, counts_s, pred)
@@ -555,7 +559,7 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
             ovf = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
         _lib.call("sg_numeric", m, n, dcode, *Aargs, ptr(kind), ptr(cap), ptr(alloc),
                   ptr(products), ptr(span_lo), ptr(span_hi), ptr(out_off), ptr(out_col), ptr(out_val),
-                  ptr(counts), ptr(ovf), ptr(skip), ptr(pred) if exact else None, ws, wsb, ctx.sp)
+                  ptr(counts), ptr(ovf), ptr(skip), ptr(pred) if exact else None, 0, ws, wsb, ctx.sp)
         if short is not None:
             overflow |= ovf
     ev[4].record(ctx.stream)
