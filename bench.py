@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-warmup", type=int, default=1,
                     help="untimed end-to-end calls first (they pin the recycled host result buffers)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0,
-                    help="target CPU time of the bounded reference sample")
+    ap.add_argument("--parity-blocks", type=int, default=8,
+                    help="row blocks of matgen.stratified_blocks the reference CPU engine runs (timed as the "
+                         "cpu_baseline leg, and compared entry by entry with this run's C)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -125,58 +126,209 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def rows_slice(a, lo, hi):
-    """Host CSR of rows [lo, hi) of a (same column space)."""
-    from paper_2604_19004_b200.csr import CsrMatrix
-    s, e = int(a.row_ptr[lo]), int(a.row_ptr[hi])
-    return CsrMatrix(hi - lo, a.ncols, a.row_ptr[lo:hi + 1] - s, a.col_idx[s:e], a.values[s:e])
+class CpuReference:
+    """The reference's own CPU engine, timed on this host's cores.
 
+    ``baseline/_ref`` holds the unmodified reference package
+    (``pip install --target baseline/_ref /root/reference/pkg``, see
+    DESIGN.md); it is imported from there (kind "reference").  When it is
+    absent the oracle port of the same engine is used (kind "port").
 
-def row_products(a, b):
-    """Intermediate products per row of A (host, for sharding and sampling)."""
-    cum = np.r_[0, np.cumsum(np.diff(b.row_ptr)[a.col_idx])]
-    return cum[a.row_ptr[1:]] - cum[a.row_ptr[:-1]]
+    R-MAT-20's whole product needs ~0.9 TB of host memory in the reference,
+    so the full-matrix time is extrapolated from row blocks
+    (``matgen.stratified_blocks``; rows are independent, engine.py:13-14):
+    the per-call fixed cost -- row statistics over all of A, B's sketches,
+    the sampled CR and the workflow choice (engine.py:147-174) -- is timed
+    once on the whole matrix, and every block runs the rest of the pipeline
+    (predict .. compact, engine.py:177-216) with the whole matrix's workflow
+    forced, so  T_full = T_fixed + sum(T_block) * total / sum(products_block).
+    """
 
+    def __init__(self, workers):
+        self.workers = workers
+        path = os.path.join(ROOT, "baseline", "_ref")
+        self.sg = None
+        if os.path.isdir(os.path.join(path, "sketchgemm")):
+            if path not in sys.path:
+                sys.path.insert(0, path)
+            try:
+                import sketchgemm
+                self.sg = sketchgemm
+            except Exception:  # reported as kind "port"
+                self.sg = None
+        self.kind = "reference" if self.sg is not None else "port"
+        if self.sg is None:
+            from oracle import ocean_cpu
+            self.oc = ocean_cpu
 
-def cpu_sample_blocks(a, b, target_products):
-    """Deterministic products-stratified row blocks: one block from the head
-    (hub rows of an unpermuted R-MAT), one from the middle and one from the
-    tail of the products prefix, each about target/3 products."""
-    per = row_products(a, b)
-    cum = np.r_[0, np.cumsum(per)]
-    total = int(cum[-1])
-    if total <= target_products:
-        return [(0, a.nrows)], total, per
-    blocks = []
-    want = max(1, target_products // 3)
-    for frac in (0.0, 0.5, 0.97):
-        start = int(np.searchsorted(cum, frac * total, side="right")) - 1
-        start = max(0, min(start, a.nrows - 1))
-        end = int(np.searchsorted(cum, cum[start] + want, side="left"))
-        end = max(start + 1, min(end, a.nrows))
-        blocks.append((start, end))
-    return blocks, total, per
+    def _csr(self, m):
+        if self.sg is None:
+            return m
+        return self.sg.CsrMatrix(m.nrows, m.ncols, np.asarray(m.row_ptr), np.asarray(m.col_idx),
+                                 np.asarray(m.values))
 
-
-def run_cpu_sample(a, b, seconds_hint, workers):
-    """Time the reference algorithm (oracle port, engine AUTO) on row blocks.
-    Returns (gflops, seconds, products_done, description)."""
-    from oracle import ocean_cpu as oc
-    # ~2.5e6 products/s/worker-ish for the numpy path; scale the sample to the hint
-    target = int(max(2e5, seconds_hint * 2.0e6 * max(1, workers) ** 0.5))
-    blocks, total, per = cpu_sample_blocks(a, b, target)
-    t = 0.0
-    done = 0
-    for lo, hi in blocks:
-        sub = rows_slice(a, lo, hi)
+    def fixed(self, a, b):
+        """(seconds, workflow) of the per-call stages on the whole matrix."""
         t0 = time.perf_counter()
-        oc.spgemm(sub, b, workers=workers)
-        t += time.perf_counter() - t0
+        if self.sg is not None:
+            from sketchgemm import analysis as an
+            A, B = self._csr(a), self._csr(b)
+            st = an.compute_row_stats(A, B)
+            avg = st.avg_products()
+            regs = an.select_registers(st.er)
+            if avg < 64:
+                wf = "upper"
+            else:
+                sk = an.build_b_sketches(B, {32: 5, 64: 6, 128: 7}[regs])
+                smp = an.sample_cr(A, sk, st, 0.03, 600, 10_000, 0)
+                wf = an.select_workflow(avg, st.er, smp.cr_hat).value  # "symbolic" / "estimate" / "upper"
+        else:
+            oc = self.oc
+            st = oc.row_stats(a, b)
+            avg = st.total / a.nrows if a.nrows else 0.0
+            regs = oc.choose_registers(st.er)
+            if avg < 64:
+                wf = "upper"
+            else:
+                sk = oc.b_sketches(b, oc.P_OF_M[regs])
+                rows = oc.sample_rows(a.nrows, oc.SAMPLE_RATIO, oc.SAMPLE_MIN, oc.SAMPLE_MAX, 0)
+                cr = oc.cr_from_sample(st.products[rows], oc.merged_estimates(a, sk, rows))
+                wf = oc.choose_workflow(avg, st.er, cr[0])
+        return time.perf_counter() - t0, wf
+
+    def whole(self, a, b):
+        """AUTO on the whole matrix: (C, seconds)."""
+        if self.sg is not None:
+            return self.sg.spgemm(self._csr(a), self._csr(b), self.sg.EngineConfig(workers=self.workers, seed=0))
+        return self.oc.spgemm(a, b, workers=self.workers)
+
+    def block(self, a, b, lo, hi, wf):
+        """(C rows [lo, hi) as host CSR, seconds of the non-fixed stages)."""
+        from paper_2604_19004_b200.matgen import rows_slice
+        sub = rows_slice(a, lo, hi)
+        if self.sg is not None:
+            ov = {"symbolic": self.sg.WorkflowOverride.FORCE_SYMBOLIC,
+                  "estimate": self.sg.WorkflowOverride.FORCE_ESTIMATE,
+                  "upper": self.sg.WorkflowOverride.FORCE_UPPER_BOUND}[wf]
+            c, rep = self.sg.spgemm(self._csr(sub), self._csr(b),
+                                    self.sg.EngineConfig(workers=self.workers, seed=0, workflow=ov))
+            ms = rep.total_ms - rep.analysis_ms - rep.sketch_ms
+        else:
+            c, rep = self.oc.spgemm(sub, b, workflow=wf, workers=self.workers)
+            ms = rep["total_ms"] - rep["analysis_ms"] - rep["sketch_ms"]
+        return c, ms / 1e3
+
+
+WHOLE_MAX_PRODUCTS = 4e8  # configs up to this size run whole in the reference (BASELINE.md §3)
+
+
+def cpu_baseline(a, b, workers, nblocks=None, budget_s=None, warmup=0, keep=False):
+    """Time the reference CPU engine on this config.
+
+    Configs of at most WHOLE_MAX_PRODUCTS products run whole (ER-10k,
+    Poisson 64^3, rect: BASELINE.md §3).  Larger ones run the blocks of
+    ``matgen.stratified_blocks`` in list order -- `warmup` untimed blocks
+    first, then timed blocks until `nblocks` are done or `budget_s` is spent
+    (at least one) -- and extrapolate (see CpuReference).  Returns a dict with
+    GFLOP/s and the sample description; the blocks' C when keep=True."""
+    from paper_2604_19004_b200 import matgen
+    ref = CpuReference(workers)
+    per = matgen.row_products(a, b)
+    total = int(per.sum())
+    if total <= WHOLE_MAX_PRODUCTS:
+        secs, outs = [], []
+        for i in range(min(warmup, 1) + max(1, min(nblocks or 3, 3))):
+            t0 = time.perf_counter()
+            c, _ = ref.whole(a, b)
+            if i >= min(warmup, 1):
+                secs.append(time.perf_counter() - t0)
+                if keep and not outs:
+                    outs.append(c)
+        t = float(np.mean(secs))
+        return {"value": 2.0 * total / t / 1e9, "unit": "GFLOP/s", "cores": workers, "kind": ref.kind,
+                "sample": f"whole matrix, AUTO workflow, mean of {len(secs)} calls ({t:.2f} s each)",
+                "extrapolated_seconds": t, "blocks": [(0, a.nrows)], "outputs": outs}
+    blocks = matgen.stratified_blocks(per)
+    t_fixed, wf = ref.fixed(a, b)
+    for i in range(warmup):
+        lo, hi = blocks[i % len(blocks)]
+        ref.block(a, b, lo, hi, wf)
+    done, t_var, used, outs = 0, 0.0, [], []
+    t_start = time.perf_counter()
+    for j in range(nblocks if nblocks is not None else len(blocks)):
+        if budget_s is not None and used and time.perf_counter() - t_start > budget_s:
+            break
+        lo, hi = blocks[j % len(blocks)]
+        c, sec = ref.block(a, b, lo, hi, wf)
+        t_var += sec
         done += int(per[lo:hi].sum())
-    desc = (f"{len(blocks)} products-stratified row blocks of A (rows "
-            + ", ".join(f"[{lo},{hi})" for lo, hi in blocks)
-            + f") = {done} products, {100.0 * done / max(total, 1):.4f}% of all {total}")
-    return 2.0 * done / t / 1e9, t, done, desc
+        used.append((lo, hi))
+        if keep:
+            outs.append(c)
+    t_full = t_fixed + t_var * total / max(done, 1)
+    uniq = sorted(set(used))
+    cover = sum(int(per[lo:hi].sum()) for lo, hi in uniq)
+    desc = (f"{len(used)} timed row blocks ({len(uniq)} distinct) of matgen.stratified_blocks, rows "
+            + ", ".join(f"[{lo},{hi})" for lo, hi in uniq[:5]) + (", ..." if len(uniq) > 5 else "")
+            + f"; {cover} distinct products = {100.0 * cover / max(total, 1):.3f}% of all {total}; "
+            f"{wf} workflow forced as AUTO picks on the whole matrix; fixed per-call stages (row stats, "
+            f"B sketches, sampled CR: engine.py:147-174) {t_fixed:.2f} s timed once on the whole matrix; "
+            f"full time = fixed + block time x total / sampled products = {t_full:.1f} s")
+    return {"value": 2.0 * total / t_full / 1e9, "unit": "GFLOP/s", "cores": workers, "kind": ref.kind,
+            "sample": desc, "workflow": wf, "fixed_seconds": t_fixed, "block_seconds": t_var,
+            "extrapolated_seconds": t_full, "blocks": used, "outputs": outs}
+
+
+def parity_rows(a, b, c, nblocks):
+    """Host copies of the rows of device C that the parity check compares:
+    the first `nblocks` stratified blocks (the whole C for configs that the
+    reference runs whole), plus the 5 rows around the 2^31 output offset."""
+    from paper_2604_19004_b200 import matgen
+    per = matgen.row_products(a, b)
+    if int(per.sum()) <= WHOLE_MAX_PRODUCTS:
+        blocks = [(0, a.nrows)]
+    else:
+        blocks = matgen.stratified_blocks(per)[:nblocks]
+    out = {blk: c.rows(*blk) for blk in blocks}
+    rp = c.row_ptr
+    if int(rp[-1]) > 2 ** 31:
+        import torch
+        r = int(torch.searchsorted(rp, torch.tensor([2 ** 31], dtype=torch.int64, device=rp.device),
+                                   right=True)[0]) - 1
+        blk = (max(0, r - 2), min(a.nrows, r + 3))
+        out[blk] = c.rows(*blk)
+    return out
+
+
+def check_parity(a, b, rows, cb):
+    """Entry-by-entry comparison of this run's C rows with the reference CPU
+    engine's output for the same rows (the reference comparator,
+    pkg/tests/matgen.py:151-156: structure exact, values rtol 1e-12, atol 0)."""
+    ref = dict(zip(cb["blocks"], cb["outputs"]))
+    extra = [blk for blk in rows if blk not in ref]
+    if extra:
+        cr = CpuReference(cb["cores"])
+        for lo, hi in extra:
+            ref[(lo, hi)], _ = cr.block(a, b, lo, hi, cb.get("workflow", "symbolic"))
+    nrows = ok_struct = 0
+    worst = 0.0
+    bad = []
+    for blk, mine in rows.items():
+        r = ref[blk]
+        same = (np.array_equal(np.asarray(mine.row_ptr), np.asarray(r.row_ptr))
+                and np.array_equal(np.asarray(mine.col_idx), np.asarray(r.col_idx)))
+        nrows += blk[1] - blk[0]
+        if not same:
+            bad.append(list(blk))
+            continue
+        ok_struct += 1
+        rv = np.asarray(r.values, dtype=np.float64)
+        if len(rv):
+            worst = max(worst, float(np.max(np.abs(np.asarray(mine.values, dtype=np.float64) - rv) / np.abs(rv))))
+    return {"blocks": len(rows), "rows": int(nrows), "structure_equal_blocks": ok_struct,
+            "max_rel_err": worst, "ok": not bad and worst <= 1e-12, "mismatched_blocks": bad,
+            "against": f"{cb['kind']} CPU engine on the same rows (structure exact, values rtol 1e-12)",
+            "row_blocks": [list(x) for x in rows]}
 
 
 TIMED_KERNELS = ("k_bmr", "k_expand", "k_hash_warp", "k_hash_block", "k_bitmap",
@@ -239,20 +391,15 @@ def main():
             return
         a, b = make_inputs(args.config)
         workers = os.cpu_count() or 1
-        vals = []
-        desc = ""
-        for i in range(args.warmup + args.steps):
-            g, sec, done, desc = run_cpu_sample(a, b, args.cpu_seconds / max(1, args.warmup + args.steps), workers)
-            if i >= args.warmup:
-                vals.append(g)
-        v = float(np.mean(vals))
+        cb = cpu_baseline(a, b, workers, nblocks=args.steps, warmup=args.warmup)
+        v = cb["value"]
         line = {"metric": metric, "value": v, "unit": "GFLOP/s", "n_gpus": n_gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, SURVEY §8d)",
+                "warmup": args.warmup, "ms_per_step": cb["extrapolated_seconds"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded generator, SURVEY §8d; values U[0.5,1.5])",
                 "impl": "reference",
-                "config": {"workload": workload, "parallelism": "cpu threads"},
-                "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": workers, "kind": "port",
-                                 "sample": desc},
+                "config": {"workload": workload, "parallelism": f"cpu threads x{workers}"},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -328,12 +475,20 @@ def main():
             stage_ms[k] = stage_ms.get(k, 0.0) + v
         nnz_c_loc = rep.nnz_c
         prod_loc = rep.total_products
-        del c
+        if _ < args.steps - 1:
+            del c
     e1.record(stream)
     torch.cuda.synchronize()
     launches = int(lib.sg_launch_count() - l0)
     ktimes = kernel_times(lib)
     lib.sg_kernel_timer(0)
+    # rows of the last timed step's C kept for the parity check against the
+    # reference CPU engine (cpu_baseline leg below): the parity row blocks
+    # plus the rows whose output offsets cross 2^31 (int64 offsets)
+    check_rows = None
+    if rank == 0 and n_gpus == 1 and not args.no_cpu:
+        check_rows = parity_rows(a, b, c, args.parity_blocks)
+    del c
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -445,11 +600,11 @@ def main():
         except Exception as exc:  # reported in the JSON line, never dropped silently
             e2e = {"value": None, "unit": "GFLOP/s", "error": f"{type(exc).__name__}: {exc}"[:300]}
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and n_gpus == 1 and not args.no_cpu:
-        g, sec, done, desc = run_cpu_sample(a, b, args.cpu_seconds, os.cpu_count() or 1)
-        cpu = {"value": g, "unit": "GFLOP/s", "cores": os.cpu_count() or 1, "kind": "port", "sample": desc,
-               "seconds": sec}
+        cb = cpu_baseline(a, b, os.cpu_count() or 1, nblocks=args.parity_blocks, keep=True)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        parity = check_parity(a, b, check_rows, cb)
 
     if rank == 0:
         line = {
@@ -464,7 +619,7 @@ def main():
                        "stage_ms": {kk: round(v, 3) for kk, v in per_step.items()},
                        "hbm_frac_whole_step": step_gbs / peak},
             "roofline": roof,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -51,10 +51,16 @@ def from_triplets_device(nrows: int, ncols: int, rows, cols, vals, device=None,
         raise ValueError("rows, cols and vals must have the same length")
     lib = _lib.load()
     stream = stream or torch.cuda.current_stream(dev)
-    ws = torch.empty(int(lib.sg_build_workspace_bytes(n)), dtype=torch.uint8, device=dev)
-    row_ptr = torch.empty(nrows + 1, dtype=torch.int64, device=dev)
-    col = torch.empty(n, dtype=torch.int32, device=dev)
-    val = torch.empty(n, dtype=dtype, device=dev)
+    if stream != torch.cuda.current_stream(dev):
+        stream.wait_stream(torch.cuda.current_stream(dev))  # inputs uploaded on the current stream
+    # allocations are made on `stream` (so the caching allocator orders
+    # their reuse after its work) and the stream is drained before the
+    # workspace is dropped
+    with torch.cuda.stream(stream):
+        ws = torch.empty(int(lib.sg_build_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+        row_ptr = torch.empty(nrows + 1, dtype=torch.int64, device=dev)
+        col = torch.empty(n, dtype=torch.int32, device=dev)
+        val = torch.empty(n, dtype=dtype, device=dev)
     nu = ctypes.c_int64(0)
     code = 0 if dtype == torch.float64 else 1
     try:
@@ -64,6 +70,8 @@ def from_triplets_device(nrows: int, ncols: int, rows, cols, vals, device=None,
         if "out of range" in str(exc):
             raise ValueError(str(exc)) from exc
         raise
+    finally:
+        stream.synchronize()
     k = int(nu.value)
     return DeviceCsr(nrows, ncols, row_ptr, col[:k], val[:k])
 
@@ -80,10 +88,17 @@ def transpose_device(a, device=None, stream=None) -> DeviceCsr:
     nnz = int(ci.numel())
     lib = _lib.load()
     stream = stream or torch.cuda.current_stream(dev)
-    ws = torch.empty(int(lib.sg_build_workspace_bytes(nnz)), dtype=torch.uint8, device=dev)
-    t_ptr = torch.empty(a.ncols + 1, dtype=torch.int64, device=dev)
-    t_col = torch.empty(nnz, dtype=torch.int32, device=dev)
-    t_val = torch.empty(nnz, dtype=vv.dtype, device=dev)
-    _lib.call("sg_transpose", a.nrows, a.ncols, ptr(rp), ptr(ci), ptr(vv), 0 if vv.dtype == torch.float64 else 1,
-              ptr(t_ptr), ptr(t_col), ptr(t_val), ptr(ws), ws.numel(), stream.cuda_stream)
+    if stream != torch.cuda.current_stream(dev):
+        stream.wait_stream(torch.cuda.current_stream(dev))  # inputs uploaded on the current stream
+    with torch.cuda.stream(stream):
+        ws = torch.empty(int(lib.sg_build_workspace_bytes(nnz)), dtype=torch.uint8, device=dev)
+        t_ptr = torch.empty(a.ncols + 1, dtype=torch.int64, device=dev)
+        t_col = torch.empty(nnz, dtype=torch.int32, device=dev)
+        t_val = torch.empty(nnz, dtype=vv.dtype, device=dev)
+    try:
+        _lib.call("sg_transpose", a.nrows, a.ncols, ptr(rp), ptr(ci), ptr(vv),
+                  0 if vv.dtype == torch.float64 else 1,
+                  ptr(t_ptr), ptr(t_col), ptr(t_val), ptr(ws), ws.numel(), stream.cuda_stream)
+    finally:
+        stream.synchronize()  # the workspace is released on return
     return DeviceCsr(a.ncols, a.nrows, t_ptr, t_col, t_val)

@@ -160,6 +160,8 @@ int download_registered(void* host_dst, const void* dev_src, size_t bytes, int t
   std::mutex mu;
   std::condition_variable cv;
   std::vector<int> state(nch, 0);  // 0 pending, 1 registered, -1 failed
+  const char* ff = getenv("SG_TEST_REGISTER_FAIL");
+  const int64_t fail_from = ff ? atoll(ff) : -1;
   int64_t next = 0;
   auto reg = [&]() {
     for (;;) {
@@ -172,7 +174,8 @@ int download_registered(void* host_dst, const void* dev_src, size_t bytes, int t
       char* p = reinterpret_cast<char*>(a0) + (size_t)i * CH;
       const size_t len = std::min(CH, body - (size_t)i * CH);
       for (size_t o = 0; o < len; o += PG) p[o] = 0;  // first touch in parallel
-      const bool ok = cudaHostRegister(p, len, cudaHostRegisterDefault) == cudaSuccess;
+      // SG_TEST_REGISTER_FAIL=k: test hook, chunks >= k fail to page-lock
+      const bool ok = (fail_from < 0 || i < fail_from) && cudaHostRegister(p, len, cudaHostRegisterDefault) == cudaSuccess;
       {
         std::lock_guard<std::mutex> l(mu);
         state[i] = ok ? 1 : -1;
@@ -183,13 +186,14 @@ int download_registered(void* host_dst, const void* dev_src, size_t bytes, int t
   std::vector<std::thread> th;
   for (int j = 0; j < T; ++j) th.emplace_back(reg);
   bool failed = false;
+  int64_t unreg = -1;  // first chunk whose page lock failed: staged path from there
   for (int64_t i = 0; i < nch; ++i) {
     {
       std::unique_lock<std::mutex> l(mu);
       cv.wait(l, [&] { return state[i] != 0; });
-      if (state[i] < 0) failed = true;
+      if (state[i] < 0) unreg = i;
     }
-    if (failed) break;
+    if (unreg >= 0) break;
     const size_t off = (size_t)i * CH, len = std::min(CH, body - off);
     if (cudaMemcpyAsync(reinterpret_cast<char*>(a0) + off, src + head + off, len, cudaMemcpyDeviceToHost, cs) !=
         cudaSuccess) {
@@ -213,6 +217,12 @@ int download_registered(void* host_dst, const void* dev_src, size_t bytes, int t
     for (auto& t : un) t.join();
   }
   cudaGetLastError();
+  if (rc == SG_OK && unreg >= 0) {
+    // page locking failed (memlock limit, IOMMU, memory pressure): the rest
+    // of the body goes through the pinned staging ring instead of failing
+    const size_t off = (size_t)unreg * CH;
+    rc = download_staged(reinterpret_cast<char*>(a0) + off, src + head + off, body - off, threads, cs);
+  }
   if (rc == SG_OK && head) {
     if (cudaMemcpyAsync(dst, src, head, cudaMemcpyDeviceToHost, cs) != cudaSuccess) rc = check_cuda("head", 0);
   }

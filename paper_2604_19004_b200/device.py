@@ -30,6 +30,13 @@ class DeviceCsr:
     def nnz(self) -> int:
         return int(self.col_idx.numel())
 
+    def rows(self, lo: int, hi: int) -> CsrMatrix:
+        """Host copy of rows [lo, hi) (row_ptr rebased to 0)."""
+        rp = self.row_ptr[lo:hi + 1].cpu().numpy()
+        s, e = int(rp[0]), int(rp[-1])
+        return CsrMatrix(hi - lo, self.ncols, rp - s, self.col_idx[s:e].cpu().numpy(),
+                         self.values[s:e].cpu().numpy())
+
     def to_host(self, pool: "HostPool | None" = None) -> CsrMatrix:
         return CsrMatrix(self.nrows, self.ncols, download(self.row_ptr, pool=pool),
                          download(self.col_idx, pool=pool), download(self.values, pool=pool))

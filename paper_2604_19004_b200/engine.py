@@ -525,21 +525,40 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     exact = pred_kind == "exact"
     dcode = _dtype_code(A.values)
     Aargs = (ptr(A.row_ptr), ptr(A.col_idx), ptr(A.values), ptr(B.row_ptr), ptr(B.col_idx), ptr(B.values))
-    st_off = st_col = st_val = counts_s = None
+    st_off = st_col = st_val = counts_s = short_fb = None
     if exact and short is not None:
         # short rows: one numeric pass into a slab at their product offsets;
-        # their counts complete the exact row sizes
-        st_off = scan(ctx, torch.where(short, alloc, torch.zeros_like(alloc)))
+        # their counts complete the exact row sizes.  The staging pass uses
+        # its own plan (hash kind, table of at least 1.25 x products slots:
+        # the 0.8 load limit can never trip, whatever the tiers or coef), not
+        # the reference plan, which is recomputed below from the exact counts.
+        s_kind = torch.full_like(kind, int(PlanKind.HASH))
+        s_cap = torch.clamp(products + (products + 3) // 4 + 1, min=1)
+        st_off = scan(ctx, torch.where(short, products, torch.zeros_like(products)))
         st_total = int(st_off[-1].item())
         st_col, st_val = ctx.empty(st_total, torch.int32), ctx.empty(st_total, dtype)
         counts_s = ctx.empty(m, torch.int64)
-        _lib.call("sg_numeric", m, n, dcode, *Aargs, ptr(kind), ptr(cap), ptr(alloc),
+        s_ovf = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
+        _lib.call("sg_numeric", m, n, dcode, *Aargs, ptr(s_kind), ptr(s_cap), ptr(products),
                   ptr(products), ptr(span_lo), ptr(span_hi), ptr(st_off), ptr(st_col), ptr(st_val),
-                  ptr(counts_s), ptr(overflow), ptr((~short).to(torch.int32)), None, SHORT_ROW_ESCR,
+                  ptr(counts_s), ptr(s_ovf), ptr((~short).to(torch.int32)), None, SHORT_ROW_ESCR,
                   ws, wsb, ctx.sp)
-        if bool(overflow[short].any()):  # cannot happen: slots hold every product
+        del s_kind, s_cap
+        if bool(s_ovf[short].any()):  # cannot happen: slots hold every product
             raise RuntimeError("internal: a staged short row overflowed its product-sized slot")
         pred = torch.where(short, counts_s, pred)
+        # the reference plan (accumulate.py:104-181) on the exact counts of
+        # every row; a staged row the reference would overflow (count over
+        # its tier limit) or plan as FALLBACK is flagged so the report counts
+        # it (engine.py:202-203, 242) -- its values are already staged
+        _lib.call("sg_plan", m, _PRED_CODE[pred_kind], ptr(pred), ptr(products), ptr(span_lo), ptr(span_hi),
+                  ts, ptr(kind), ptr(cap), ptr(alloc), ctx.sp)
+        lim = torch.where((kind == int(PlanKind.HASH)) | (kind == int(PlanKind.ENHANCED_HASH)),
+                          (cap.to(torch.float64) * 0.8).floor().to(torch.int64),
+                          torch.where(kind == int(PlanKind.DENSE), alloc, torch.full_like(alloc, 1 << 62)))
+        s_over = short & ((kind == int(PlanKind.FALLBACK)) | (counts_s > lim))
+        overflow |= s_over.to(torch.uint8)
+        short_fb = s_over
     if exact:
         row_ptr = scan(ctx, pred)
         nnz_c = int(row_ptr[-1].item()) if m else 0
@@ -596,7 +615,14 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         wstats = {"rows": int(wrow.sum()), "windows": win.total, "nnz_a": int(al[wrow].sum()),
                   "products": int(products[wrow].sum()), "nnz_c": int(rl[wrow].sum()),
                   "saved_bitmaps": win.bm_save is not None}
-    rest, n_rest = (fb_rows, n_fb) if win is None else select_fallback(ctx, m, kind, products, overflow, win.nwin)
+    if short_fb is not None:
+        # staged rows the reference would rerun already hold their values
+        excl = ((win.nwin[:m] > 0) | short_fb).to(torch.int32)
+        rest, n_rest = select_fallback(ctx, m, kind, products, overflow, excl)
+    elif win is None:
+        rest, n_rest = fb_rows, n_fb
+    else:
+        rest, n_rest = select_fallback(ctx, m, kind, products, overflow, win.nwin)
     if n_rest:
         _lib.call("sg_fallback", 1, n_rest, ptr(rest), n, dcode, *fargs, ptr(row_ptr),
                   ptr(C_col), ptr(C_val), ptr(counts), None, ws, wsb, ctx.sp)

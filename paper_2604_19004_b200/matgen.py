@@ -106,3 +106,51 @@ def make_config(name: str):
         a = rmat(int(name[4:]))
         return a, a
     raise ValueError(f"unknown config {name!r}")
+
+
+def row_products(a, b) -> np.ndarray:
+    """Intermediate products per row of A·B (analysis.py:100-104), host side,
+    for choosing sample blocks (input preparation, not the multiply)."""
+    cum = np.r_[0, np.cumsum(np.diff(np.asarray(b.row_ptr))[np.asarray(a.col_idx)])]
+    rp = np.asarray(a.row_ptr)
+    return cum[rp[1:]] - cum[rp[:-1]]
+
+
+def stratified_blocks(per_row: np.ndarray, nblocks: int = 20, block_frac: float = 1e-3) -> list:
+    """Deterministic products-stratified row blocks of A.
+
+    Block s starts at the row holding product number s/nblocks x total (so
+    block 0 starts at row 0: the hub rows of an unpermuted R-MAT) and takes
+    whole rows until it holds block_frac x total products (at least one row).
+    The same list drives the CPU-reference sample (bench.py), the sampled-row
+    parity check of the bench's own output, and the config-scale GPU parity
+    tests (fixtures: tests/golden/make_config_golden.py).  Valid as a parity
+    sample because Gustavson rows are independent (PAPER.md:153,
+    engine.py:13-14)."""
+    per = np.asarray(per_row, dtype=np.int64)
+    m = len(per)
+    cum = np.r_[0, np.cumsum(per)]
+    total = int(cum[-1])
+    if m == 0 or total == 0:
+        return [(0, m)] if m else []
+    target = max(1, int(total * block_frac))
+    out = []
+    for s in range(nblocks):
+        start = int(np.searchsorted(cum, s * total // nblocks, side="right")) - 1
+        start = max(0, min(start, m - 1))
+        end = int(np.searchsorted(cum, cum[start] + target, side="left"))
+        end = max(start + 1, min(end, m))
+        if out and start < out[-1][1]:
+            start = out[-1][1]
+            if start >= m:
+                break
+            end = max(end, start + 1)
+        out.append((start, end))
+    return out
+
+
+def rows_slice(a, lo: int, hi: int):
+    """Host CSR of rows [lo, hi) of a (same column space)."""
+    rp = np.asarray(a.row_ptr)
+    s, e = int(rp[lo]), int(rp[hi])
+    return CsrMatrix(hi - lo, a.ncols, rp[lo:hi + 1] - s, np.asarray(a.col_idx)[s:e], np.asarray(a.values)[s:e])

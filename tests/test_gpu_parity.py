@@ -235,6 +235,21 @@ def test_download_large_ragged(gpu):
         assert int(out.sum()) == int(t.sum().item())
 
 
+def test_download_register_failure_falls_back(gpu, monkeypatch):
+    """A page-lock failure part way through a registered download finishes
+    through the staged ring instead of failing (sg_io.cu download_registered)."""
+    from paper_2604_19004_b200.device import download
+    n = (600 << 20) // 8 + 777  # > 2 registered 256 MB chunks
+    t = torch.arange(n, dtype=torch.int64, device=gpu) * 5 + 3
+    for k in ("0", "1"):
+        monkeypatch.setenv("SG_TEST_REGISTER_FAIL", k)
+        out = download(t, 4)
+        assert out.shape == (n,)
+        np.testing.assert_array_equal(out[:3], [3, 8, 13])
+        assert int(out[-1]) == (n - 1) * 5 + 3
+        assert int(out.sum()) == int(t.sum().item())
+
+
 def test_host_pool_results_recycled(gpu):
     """EngineConfig(host_pool=True): results land in pinned pool buffers that
     return to the pool when dropped and are reused by the next call."""
@@ -297,6 +312,34 @@ def test_staged_short_rows(gpu, monkeypatch, force):
     C, rep = spgemm(a, b, EngineConfig())
     assert rep.workflow == rrep["workflow"] == "symbolic"
     assert rep.kernel_ms["compact"] >= 0.0
+    np.testing.assert_array_equal(C.row_ptr, ref.row_ptr)
+    np.testing.assert_array_equal(C.col_idx, ref.col_idx)
+    np.testing.assert_allclose(C.values, ref.values, rtol=1e-12, atol=0)
+    assert rep.overflow_row_count == rrep["overflow_row_count"]
+
+
+@pytest.mark.parametrize("variant", ["tiny_tiers", "coef1", "coef1.1"])
+def test_staged_short_rows_custom_tiers(gpu, variant):
+    """Staged short rows (low-CR symbolic workflow) with tiers / coef under
+    which the reference plans short rows as FALLBACK or overflows them
+    (tiny tiers as test_engine.py:280-292; coef < 1.25 puts a row's distinct
+    count over 0.8 x its table).  C and the overflow count equal the oracle's."""
+    from paper_2604_19004_b200 import EngineConfig, TierConfig, spgemm
+    from oracle import ocean_cpu as oc
+    rng = np.random.default_rng(11)
+    a = oc.triplets_to_csr(3000, 2000, np.repeat(np.arange(3000), 16), rng.integers(0, 2000, 48000),
+                           rng.uniform(0.5, 1.5, 48000))
+    b = oc.triplets_to_csr(2000, 900_000, np.repeat(np.arange(2000), 16), rng.integers(0, 900_000, 32000),
+                           rng.uniform(0.5, 1.5, 32000))
+    if variant == "tiny_tiers":
+        tiers = TierConfig(hash_capacities=(8, 16), enhanced_hash_capacity=24, dense_spans=(16, 32))
+        ref, rrep = oc.spgemm(a, b, tiers=tiers)
+        C, rep = spgemm(a, b, EngineConfig(tiers=tiers))
+    else:
+        coef = float(variant[4:])
+        ref, rrep = oc.spgemm(a, b, coef=coef)
+        C, rep = spgemm(a, b, EngineConfig(coef=coef))
+    assert rep.workflow == rrep["workflow"] == "symbolic"
     np.testing.assert_array_equal(C.row_ptr, ref.row_ptr)
     np.testing.assert_array_equal(C.col_idx, ref.col_idx)
     np.testing.assert_allclose(C.values, ref.values, rtol=1e-12, atol=0)
