@@ -55,7 +55,7 @@ struct Csr {
 // compacted non-empty A entries of one chunk (shared memory)
 struct Entries {
   int64_t* S;   // first product index of the entry within the chunk (excl scan)
-  int64_t* bs;  // start of the B row
+  int64_t* d;   // B position of product p of this entry is p + d (B row start - S)
   double* av;   // A value
 };
 
@@ -92,7 +92,7 @@ __device__ __forceinline__ void plan_load(const Entries& E, int nent, int64_t p0
   const int64_t seg_end = (c0 + 1 < nent) ? E.S[c0 + 1] : (int64_t)NOLIMIT;
   B.valid = 0;
   if (seg_end >= blk_end) {
-    const int64_t base = E.bs[c0] + (p0 - E.S[c0]) + lane;
+    const int64_t base = E.d[c0] + p0 + lane;
     const double a = VALUES ? E.av[c0] : 0.0;
     const int nvalid = (int)(blk_end - p0) - lane;
     const int32_t* cp = b_col + base;
@@ -121,7 +121,7 @@ __device__ __forceinline__ void plan_load(const Entries& E, int nent, int64_t p0
     const int c = c0 + __popc(mask & le);
     const int64_t p = q0 + lane;
     cc[u] = c;
-    jj[u] = (p < pend) ? E.bs[c] + (p - E.S[c]) : -1;
+    jj[u] = (p < pend) ? E.d[c] + p : -1;
     const int k = __popc(mask);
     const int64_t nk = __shfl_sync(SG_FULL, nxt, k);
     c0 = c0 + k + (nk == q0 + 32 ? 1 : 0);
@@ -191,6 +191,78 @@ __device__ __forceinline__ void warp_products(const Entries& E, int nent, int64_
   }
 }
 
+// Block-wide product iteration over a chunk's compacted entries (E.S strictly
+// increasing exclusive product prefix, E.d, E.av), products [0, P).
+// Products are cut into 32-product groups; a group table built once per
+// sub-chunk holds, per group, the entry owning its first product and a
+// bitmask of the entries starting inside it, so a lane finds its product's
+// entry with one broadcast load and a popcount -- no per-step owner search,
+// no dependency between steps (every warp keeps UNR groups of gathers in
+// flight).  Sub-chunks of GRP_MAX groups bound the table.
+#ifndef SG_GROUPED
+#define SG_GROUPED 1
+#endif
+constexpr int GRP_MAX = 512;
+// one table per kernel that iterates (file-scope shared: not duplicated per
+// template instantiation of block_products)
+__shared__ int2 g_grp[GRP_MAX];
+
+template <bool VALUES, typename V, class Op>
+__device__ __forceinline__ void block_products(const Entries& E, int nent, int64_t P,
+                                               const int32_t* __restrict__ b_col,
+                                               const V* __restrict__ b_val, Op& op) {
+  int2* grp = g_grp;
+  const int nw = blockDim.x >> 5, w = warp_id(), lane = lane_id();
+  const unsigned le = lanemask_le();
+  constexpr int U = SG_UNR;
+  for (int64_t base = 0; base < P; base += 32 * (int64_t)GRP_MAX) {
+    const int ng = (int)min((int64_t)GRP_MAX, (P - base + 31) >> 5);
+    for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+      const int64_t q = base + 32 * (int64_t)g;
+      int lo = 0, hi = nent - 1;  // last entry with S <= q
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (E.S[mid] <= q) lo = mid; else hi = mid - 1;
+      }
+      unsigned mask = 0;
+      for (int c = lo + 1; c < nent; ++c) {
+        const int64_t dd = E.S[c] - q;
+        if (dd >= 32) break;
+        mask |= 1u << (unsigned)dd;
+      }
+      grp[g] = make_int2(lo, (int)mask);
+    }
+    __syncthreads();
+    for (int g0 = w * U; g0 < ng; g0 += nw * U) {
+      int32_t col[U];
+      double v[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int g = g0 + u;
+        ok[u] = false;
+        col[u] = 0;
+        v[u] = 0.0;
+        if (g < ng) {
+          const int2 gr = grp[g];
+          const int c = gr.x + __popc((unsigned)gr.y & le);
+          const int64_t p = base + 32 * (int64_t)g + lane;
+          if (p < P) {
+            const int64_t pos = E.d[c] + p;
+            ok[u] = true;
+            col[u] = __ldg(b_col + pos);
+            if (VALUES) v[u] = E.av[c] * (double)__ldg(b_val + pos);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ok[u]) op(col[u], v[u]);
+    }
+    __syncthreads();
+  }
+}
+
 // Load one chunk of A entries for a warp (CH = 32), compacting empties.
 // Returns the chunk's product total; nent receives the entry count.
 template <bool VALUES, typename V>
@@ -212,7 +284,7 @@ __device__ __forceinline__ int64_t warp_load_chunk(int64_t t, int64_t t1, const 
   __syncwarp();
   if (len > 0) {
     E.S[pos] = incl - len;
-    E.bs[pos] = bs;
+    E.d[pos] = bs - (incl - len);
     if (VALUES) E.av[pos] = av;
   }
   __syncwarp();
@@ -263,14 +335,20 @@ __device__ __forceinline__ void block_row(int64_t row, const int64_t* __restrict
     const int64_t S = ex >> 12, pos = ex & 4095, P = tot >> 12, nent64 = tot & 4095;
     if (len > 0) {
       E.S[pos] = S;
-      E.bs[pos] = bs;
+      E.d[pos] = bs - S;
       if (VALUES) E.av[pos] = av;
     }
     __syncthreads();
+#if SG_GROUPED
+    (void)nw;
+    (void)w;
+    block_products<VALUES, V>(E, (int)nent64, P, b_col, b_val, op);
+#else
     const int64_t per = ((P + nw - 1) / nw + 31) & ~(int64_t)31;
     const int64_t pb = min(P, per * w), pe = min(P, per * (w + 1));
     warp_products<VALUES, V>(E, (int)nent64, pb, pe, b_col, b_val, op);
     __syncthreads();
+#endif
     if (stop && *stop) return;
   }
 }
@@ -845,7 +923,7 @@ __global__ void __launch_bounds__(ESC_WARPS * 32) k_esc(int64_t nbin, const int3
       if (p < P) {
         int c = 0;
         while (c + 1 < nent && E.S[c + 1] <= p) ++c;
-        const int64_t j = E.bs[c] + (p - E.S[c]);
+        const int64_t j = E.d[c] + p;
         const int pos = np + (int)p;
         if (pos < 64) {
           key[w][pos] = ((unsigned long long)(uint32_t)B.col[j] << 32) | (unsigned)pos;
@@ -1188,9 +1266,13 @@ template <bool VALUES, typename V, class Op>
 __device__ __forceinline__ void block_chunk_products(const Entries& E, int nent, int64_t P,
                                                      const int32_t* __restrict__ b_col,
                                                      const V* __restrict__ b_val, Op& op) {
+#if SG_GROUPED
+  block_products<VALUES, V>(E, nent, P, b_col, b_val, op);
+#else
   const int nw = blockDim.x >> 5, w = warp_id();
   const int64_t per = ((P + nw - 1) / nw + 31) & ~(int64_t)31;
   warp_products<VALUES, V>(E, nent, min(P, per * w), min(P, per * (w + 1)), b_col, b_val, op);
+#endif
 }
 
 // The window's key set lives in shared memory as interleaved 32-bit words
@@ -1355,7 +1437,7 @@ __device__ __forceinline__ int64_t block_load_tiles(int64_t t, int64_t t1, int32
   const int64_t S = ex >> 12, pos = ex & 4095, P = tot >> 12, n64 = tot & 4095;
   if (len > 0) {
     E.S[pos] = S;
-    E.bs[pos] = bs;
+    E.d[pos] = bs - S;
     if (VALUES) E.av[pos] = av;
   }
   __syncthreads();
