@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="rmat20")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--workflow", default="auto", choices=["auto", "symbolic", "estimate", "upper"],
+                    help="WorkflowOverride of every step (estimate = FORCE_ESTIMATE: the HLL-estimate-driven "
+                         "workflow, reference engine.py:166-171)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-warmup", type=int, default=1,
                     help="untimed end-to-end calls first (they pin the recycled host result buffers)")
@@ -49,6 +52,9 @@ def parse():
                     help="row blocks of matgen.stratified_blocks the reference CPU engine runs (timed as the "
                          "cpu_baseline leg, and compared entry by entry with this run's C)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--batch-products", type=float, default=None,
+                    help="N>1: rows of each rank run in batches of at most this many products (default: "
+                         "4e9 for R-MAT-23, whose C does not fit in HBM; none otherwise)")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -417,17 +423,25 @@ def main():
         torch.cuda.set_device(local)
         backend = os.environ.get("SG_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # NCCL's own log shows the communicator (nranks, NVLS / NVLink
+            # transport) on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     lib = _lib.load()
-    a, b = make_inputs(args.config)
+    # the root builds the inputs; under torchrun the other ranks receive them
+    # over NCCL (plan_shards), so they skip the host generation
+    a, b = make_inputs(args.config) if (world == 1 or rank == 0) else (None, None)
     same = b is a
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     vbytes = 8 if args.dtype == "f64" else 4
-    cfg = EngineConfig(return_device=True, dtype=args.dtype)
+    from paper_2604_19004_b200 import WorkflowOverride
+    wf_over = WorkflowOverride(args.workflow)
+    cfg = EngineConfig(return_device=True, dtype=args.dtype, workflow=wf_over)
     if n_gpus == 1:
         a_loc = a
         A = to_device(a, dev, dt)
@@ -436,16 +450,30 @@ def main():
         def step():
             return spgemm(A, B, cfg)
     else:
-        # row-sharded job (shard.py): every step broadcasts B from rank 0
-        # over NCCL, cuts A's rows by balanced products (row-stats kernel on
-        # rank 0), multiplies the local rows, and exchanges nnz offsets
-        from paper_2604_19004_b200.shard import gpu_local_fn, gpu_products_fn, spgemm_sharded
+        # row-sharded job (shard.py), planned ONCE outside the timed loop:
+        # B (= A) broadcast from rank 0 over NCCL, A's rows cut by balanced
+        # products (row-stats kernel on rank 0), the workflow decided once
+        # for the whole product on rank 0 and broadcast.  A step multiplies
+        # the local rows (in product-bounded batches when C does not fit the
+        # GPU: R-MAT-23) and exchanges nnz offsets; no data-path collective.
+        from paper_2604_19004_b200.shard import (gpu_decide_fn, gpu_local_fn, gpu_products_fn, plan_shards,
+                                                 run_shard)
         A0 = to_device(a, dev, dt) if rank == 0 else None
         B0 = (A0 if same else to_device(b, dev, dt)) if rank == 0 else None
+        budget = args.batch_products or (4e9 if a.nnz > 50_000_000 else None)
+        plan = plan_shards(A0, B0, device=dev, products_fn=gpu_products_fn(dev),
+                           decide_fn=gpu_decide_fn(cfg, dev), batch_products=budget)
+        del A0, B0
         local_fn = gpu_local_fn(cfg)
+        checks = torch.zeros(2, dtype=torch.float64, device=dev)
+
+        def consume(lo, hi, rp, ci, vv):
+            # C batches that do not stay resident leave a checksum
+            checks[0] += vv.double().sum()
+            checks[1] += ci.double().sum()
 
         def step():
-            sh = spgemm_sharded(A0, B0, local_fn, device=dev, gather=False, products_fn=gpu_products_fn(dev))
+            sh = run_shard(plan, local_fn, consume=consume if len(plan.batches) > 1 else None)
             return sh, sh.report
 
         a_loc = None
@@ -475,6 +503,7 @@ def main():
             stage_ms[k] = stage_ms.get(k, 0.0) + v
         nnz_c_loc = rep.nnz_c
         prod_loc = rep.total_products
+        c_last_local = getattr(c, "local", None)
         if _ < args.steps - 1:
             del c
     e1.record(stream)
@@ -495,19 +524,19 @@ def main():
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms, nnz_c_loc, prod_loc], dtype=torch.float64, device=dev)
     if world > 1:
-        mx = t.clone()
-        dist.all_reduce(mx[0:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:3], op=dist.ReduceOp.SUM)
-        t[0] = mx[0]
+        # the stitched report already holds whole-product nnz_c / products
+        # (run_shard sums them over ranks); time is the max over ranks
+        dist.all_reduce(t[0:1], op=dist.ReduceOp.MAX)
+        nnz_c_loc, prod_loc = c_last_local["nnz_c"], c_last_local["products"]
     ms_tot, nnz_c, products = float(t[0]), int(t[1]), int(t[2])
     ms_step = ms_tot / args.steps
     gflops = 2.0 * products / (ms_step * 1e-3) / 1e9
 
     # roofline of the dominant stage on this rank (CUDA events on the launch stream)
     peak, peak_kind = load_peaks()
-    m, k = a.nrows, b.nrows
-    loc_rows = rep.nrows_local if hasattr(rep, "nrows_local") else (a_loc.nrows if a_loc is not None else m // n_gpus)
-    loc_nnz = a_loc.nnz if a_loc is not None else a.nnz // n_gpus
+    m, k = (a.nrows, b.nrows) if a is not None else (plan.A[0], plan.B[0])
+    loc_rows = a_loc.nrows if a_loc is not None else c_last_local["rows"]
+    loc_nnz = a_loc.nnz if a_loc is not None else c_last_local["nnz_a"]
     alg = compulsory_bytes(loc_rows, k, loc_nnz, prod_loc, nnz_c_loc, vbytes)
     per_step = {kk: v / args.steps for kk, v in stage_ms.items() if kk != "h2d"}
     dom = max(per_step, key=per_step.get) if per_step else "numeric"
@@ -557,11 +586,14 @@ def main():
     # e2e through the public API with host buffers (H2D + D2H inside the timed region)
     e2e = None
     torch.cuda.empty_cache()
-    if not args.no_e2e:
+    if not args.no_e2e and n_gpus > 1 and len(plan.batches) > 1:
+        e2e = {"value": None, "unit": "GFLOP/s",
+               "skipped": "C does not fit in host memory (R-MAT-23: ~2 TB); batches are checksummed on device"}
+    elif not args.no_e2e:
         try:
-            cfg_h = EngineConfig(dtype=args.dtype, host_pool=True)
-            a_h = a if args.dtype == "f64" else a.astype(np.float32)
-            b_h = (a_h if same else (b if args.dtype == "f64" else b.astype(np.float32)))
+            cfg_h = EngineConfig(dtype=args.dtype, host_pool=True, workflow=wf_over)
+            a_h = a if (a is None or args.dtype == "f64") else a.astype(np.float32)
+            b_h = (a_h if same else (b if (b is None or args.dtype == "f64") else b.astype(np.float32)))
             ts = []
             cbytes = 0
             from paper_2604_19004_b200.device import HOST_POOL
@@ -574,9 +606,10 @@ def main():
                 else:
                     from paper_2604_19004_b200.device import download
                     from paper_2604_19004_b200.shard import gpu_local_fn, gpu_products_fn, spgemm_sharded
+                    from paper_2604_19004_b200.shard import gpu_decide_fn
                     sh = spgemm_sharded(a_h if rank == 0 else None, b_h if rank == 0 else None,
                                         gpu_local_fn(cfg), device=dev, gather=False,
-                                        products_fn=gpu_products_fn(dev))
+                                        products_fn=gpu_products_fn(dev), decide_fn=gpu_decide_fn(cfg, dev))
                     ch = [download(sh.row_ptr, pool=HOST_POOL), download(sh.col_idx, pool=HOST_POOL),
                           download(sh.values, pool=HOST_POOL)]
                     cbytes = sum(x.nbytes for x in ch)
@@ -584,8 +617,8 @@ def main():
                 if it >= args.e2e_warmup:
                     ts.append(time.perf_counter() - t0)
                 del ch
-            h2d = a_h.row_ptr.nbytes + a_h.col_idx.nbytes + a_h.values.nbytes
-            if b_h is not a_h:
+            h2d = (a_h.row_ptr.nbytes + a_h.col_idx.nbytes + a_h.values.nbytes) if a_h is not None else 0
+            if b_h is not a_h and b_h is not None:
                 h2d += b_h.row_ptr.nbytes + b_h.col_idx.nbytes + b_h.values.nbytes
             if n_gpus > 1 and rank != 0:
                 h2d = 0  # only the root uploads; the others receive over NVLink
@@ -616,7 +649,16 @@ def main():
                        "products": products, "nnz_c": nnz_c, "parallelism": f"row-shard x{n_gpus}",
                        "l2": "no flush needed: every step writes C (>> 126 MB L2)",
                        "workflow": rep.workflow if rep else None,
+                       "workflow_override": args.workflow,
                        "stage_ms": {kk: round(v, 3) for kk, v in per_step.items()},
+                       "shard_rank0": c_last_local if n_gpus > 1 else None,
+                       "c_checksum": ([float(x) for x in checks.tolist()] if (n_gpus > 1 and len(plan.batches) > 1)
+                                      else None),
+                       # north star: sketch + sampled CR + (estimate workflow) all-row estimate,
+                       # as a share of the whole step
+                       "estimation_share": ((per_step.get("sketch", 0.0)
+                                             + (per_step.get("predict", 0.0) if rep and rep.workflow == "estimate"
+                                                else 0.0)) / ms_step) if ms_step else None,
                        "hbm_frac_whole_step": step_gbs / peak},
             "roofline": roof,
             "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "gpu_launches": launches, "clocks": clk,

@@ -119,6 +119,10 @@ class EngineConfig:
     # symbolic workflow: rows of <= 1024 products skip the count pass and are
     # accumulated once into a product-sized staging slab, then compacted
     stage_short_rows: bool = True
+    # multi-GPU: the workflow decision of the WHOLE product, made once on the
+    # root rank (shard.Decision); a shard then skips its own sampling and
+    # reports the global er / cr_hat / workflow / registers
+    decision: object | None = None
 
     def __post_init__(self):
         if self.registers is not None and self.registers not in PRECISION_FOR:

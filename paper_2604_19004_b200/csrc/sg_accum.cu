@@ -26,6 +26,7 @@
 // range of products (CREDUX.OR finds segment owners), so a row with one hub
 // B row keeps all warps busy.
 #include <array>
+#include <type_traits>
 #include <map>
 #include <mutex>
 #include <algorithm>
@@ -207,16 +208,35 @@ constexpr int GRP_MAX = 512;
 // template instantiation of block_products)
 __shared__ int2 g_grp[GRP_MAX];
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint2 lds_v2u32(uint32_t a) {
+  uint2 r;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ int64_t lds_s64(uint32_t a) {
+  int64_t r;
+  asm volatile("ld.shared.s64 %0, [%1];" : "=l"(r) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double r;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(a));
+  return r;
+}
+
 template <bool VALUES, typename V, class Op>
 __device__ __forceinline__ void block_products(const Entries& E, int nent, int64_t P,
                                                const int32_t* __restrict__ b_col,
                                                const V* __restrict__ b_val, Op& op) {
   int2* grp = g_grp;
+  const uint32_t grp_s = smem_u32(g_grp), d_s = smem_u32(E.d), av_s = smem_u32(E.av);
   const int nw = blockDim.x >> 5, w = warp_id(), lane = lane_id();
   const unsigned le = lanemask_le();
   constexpr int U = SG_UNR;
   for (int64_t base = 0; base < P; base += 32 * (int64_t)GRP_MAX) {
-    const int ng = (int)min((int64_t)GRP_MAX, (P - base + 31) >> 5);
+    const int rem = (int)min((int64_t)32 * GRP_MAX, P - base);  // products of this sub-chunk
+    const int ng = (rem + 31) >> 5;
     for (int g = threadIdx.x; g < ng; g += blockDim.x) {
       const int64_t q = base + 32 * (int64_t)g;
       int lo = 0, hi = nent - 1;  // last entry with S <= q
@@ -233,31 +253,43 @@ __device__ __forceinline__ void block_products(const Entries& E, int nent, int64
       grp[g] = make_int2(lo, (int)mask);
     }
     __syncthreads();
+    const int32_t* bc = b_col + base;  // product p of the sub-chunk is at d + p
+    const V* bv = b_val + base;
     for (int g0 = w * U; g0 < ng; g0 += nw * U) {
       int32_t col[U];
       double v[U];
-      bool ok[U];
+      if ((g0 + U) * 32 <= rem) {
+        // full step: U groups, every lane has a product (no predicates)
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int g = g0 + u;
-        ok[u] = false;
-        col[u] = 0;
-        v[u] = 0.0;
-        if (g < ng) {
-          const int2 gr = grp[g];
-          const int c = gr.x + __popc((unsigned)gr.y & le);
-          const int64_t p = base + 32 * (int64_t)g + lane;
-          if (p < P) {
-            const int64_t pos = E.d[c] + p;
-            ok[u] = true;
-            col[u] = __ldg(b_col + pos);
-            if (VALUES) v[u] = E.av[c] * (double)__ldg(b_val + pos);
+        for (int u = 0; u < U; ++u) {
+          const uint2 gr = lds_v2u32(grp_s + (uint32_t)(g0 + u) * 8u);
+          const uint32_t c = gr.x + (uint32_t)__popc(gr.y & le);
+          const int64_t pos = lds_s64(d_s + c * 8u) + (int64_t)((g0 + u) * 32 + lane);
+          col[u] = __ldg(bc + pos);
+          if (VALUES) v[u] = lds_f64(av_s + c * 8u) * (double)__ldg(bv + pos);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) op(col[u], VALUES ? v[u] : 0.0);
+      } else {
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int p = (g0 + u) * 32 + lane;
+          ok[u] = p < rem;
+          col[u] = 0;
+          v[u] = 0.0;
+          if (ok[u]) {
+            const uint2 gr = lds_v2u32(grp_s + (uint32_t)(g0 + u) * 8u);
+            const uint32_t c = gr.x + (uint32_t)__popc(gr.y & le);
+            const int64_t pos = lds_s64(d_s + c * 8u) + (int64_t)p;
+            col[u] = __ldg(bc + pos);
+            if (VALUES) v[u] = lds_f64(av_s + c * 8u) * (double)__ldg(bv + pos);
           }
         }
-      }
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (ok[u]) op(col[u], v[u]);
+        for (int u = 0; u < U; ++u)
+          if (ok[u]) op(col[u], v[u]);
+      }
     }
     __syncthreads();
   }
@@ -1306,28 +1338,17 @@ struct WinSetOp {
   }
 };
 
+
 struct WinAddOp {
   uint32_t wp;    // shared address of the uint2 words
   uint32_t vals;  // shared address of the fp64 values
   int32_t c0;
-  __device__ __forceinline__ void operator()(int32_t col, double v) {
+  __device__ __forceinline__ uint32_t slot(int32_t col) const {
     const uint32_t x = (uint32_t)(col - c0);
-#if defined(SG_PASS2_MODE) && SG_PASS2_MODE == 4
-    // experiment: loads only (no rank, no accumulate)
-    if (v == 12345.678) smem_add_f64(vals + (x & 15) * 8, v);
-    return;
-#endif
     const uint2 p = lds_u2(wp + (x >> 5) * 8);
-    const uint32_t r = p.y + __popc(p.x & ((2u << (x & 31)) - 1u)) - 1u;
-#if defined(SG_PASS2_MODE) && SG_PASS2_MODE == 3
-    // experiment: racy plain add (wrong values, timing only)
-    double o;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(o) : "r"(vals + r * 8));
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(vals + r * 8), "d"(o + v) : "memory");
-#else
-    smem_add_f64(vals + r * 8, v);
-#endif
+    return vals + (p.y + __popc(p.x & ((2u << (x & 31)) - 1u)) - 1u) * 8u;
   }
+  __device__ __forceinline__ void operator()(int32_t col, double v) { smem_add_f64(slot(col), v); }
 };
 
 // Exclusive popcount prefix over n32 <= 2 * WIN_WORDS interleaved words in
@@ -1934,7 +1955,9 @@ __global__ void k_classify_fallback(int64_t nrows, const int64_t* __restrict__ r
 
 template <class K>
 static int set_smem(K kern, size_t bytes) {
-  if (bytes > 48 * 1024) {
+  // the 48 KB default limit counts static shared memory too (the product
+  // iterator's group table and scratch): opt in well before it
+  if (bytes > 32 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) {
       set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));

@@ -24,7 +24,7 @@ from __future__ import annotations
 import ctypes
 import threading
 import time
-from dataclasses import replace
+from dataclasses import dataclass, replace
 
 import numpy as np
 import torch
@@ -369,6 +369,56 @@ def select_fallback(ctx: _Ctx, m, kind, products, overflow, exclude):
     return rows[:n], n
 
 
+@dataclass(frozen=True)
+class Decision:
+    """Workflow decision of one whole product (engine.py:147-174), made once
+    on the root rank and applied by every shard (EngineConfig.decision)."""
+
+    workflow: str          # WorkflowKind value
+    registers: int
+    er: float
+    cr: tuple | None       # (cr_hat, mean row CR, std row CR) of the sample
+    total_products: int
+
+
+def decide(a, b, cfg: EngineConfig | None = None, device=None) -> Decision:
+    """Analysis + sketch/sample stages of spgemm on the whole operands: the
+    same row statistics, seeded sample and selection rules as the engine."""
+    cfg = cfg or EngineConfig()
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    stream = torch.cuda.current_stream(device)
+    with torch.cuda.device(device), torch.cuda.stream(stream):
+        ctx = _Ctx(device, stream)
+        A = to_device(a, device)
+        B = A if b is a else to_device(b, device)
+        products, _, _, totals = row_stats(ctx, A, B)
+        total = int(totals.cpu()[0])
+        m = A.nrows
+        er = total / A.nnz if A.nnz else 0.0
+        avg = total / m if m else 0.0
+        registers = cfg.registers if cfg.registers is not None else select_registers(er)
+        W = cfg.workflow
+        cr = None
+        if W is WorkflowOverride.FORCE_SYMBOLIC:
+            wf = WorkflowKind.SYMBOLIC
+        elif W is WorkflowOverride.FORCE_UPPER_BOUND or (W is WorkflowOverride.AUTO and avg < 64):
+            wf = WorkflowKind.UPPER_BOUND
+        else:
+            p = PRECISION_FOR[registers]
+            regs = hll_build(ctx, B, p)
+            if m == 0:
+                cr = (1.0, 1.0, 0.0)
+            else:
+                rows_d = sample_rows_device(device, m, cfg.sample_ratio, cfg.sample_min, cfg.sample_max, cfg.seed)
+                est = hll_estimate(ctx, A, regs, p, rows_d)
+                both = torch.stack((est, products[rows_d].to(torch.float64))).cpu().numpy()
+                est_s, prods = both[0], both[1]
+                row_cr = np.where(prods > 0, prods / np.maximum(est_s, 1.0), 1.0)
+                cr = (float(prods.sum() / max(1.0, est_s.sum())), float(row_cr.mean()), float(row_cr.std()))
+            wf = WorkflowKind.HLL_ESTIMATION if W is WorkflowOverride.FORCE_ESTIMATE else select_workflow(avg, er, cr[0])
+        return Decision(wf.value, registers, er, cr, total)
+
+
 def _dtype_code(v: torch.Tensor) -> int:
     return 0 if v.dtype == torch.float64 else 1
 
@@ -433,17 +483,29 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
 
     # ---- sketch + sampled CR (engine.py:157-174)
     registers = cfg.registers if cfg.registers is not None else select_registers(er)
-    p = PRECISION_FOR[registers]
     regs = None
     cr = None
     W = cfg.workflow
-    if W is WorkflowOverride.FORCE_SYMBOLIC:
+    dec = cfg.decision
+    if dec is not None:
+        # decided once for the whole product on the root rank (shard.py)
+        registers, er = dec.registers, dec.er
+        kind_wf = WorkflowKind(dec.workflow)
+        cr = dec.cr
+        p = PRECISION_FOR[registers]
+        if kind_wf is WorkflowKind.HLL_ESTIMATION:
+            regs = hll_build(ctx, B, p)
+    elif W is WorkflowOverride.FORCE_SYMBOLIC:
+        p = PRECISION_FOR[registers]
         kind_wf = WorkflowKind.SYMBOLIC
     elif W is WorkflowOverride.FORCE_UPPER_BOUND:
+        p = PRECISION_FOR[registers]
         kind_wf = WorkflowKind.UPPER_BOUND
     elif W is WorkflowOverride.AUTO and avg < 64:
+        p = PRECISION_FOR[registers]
         kind_wf = WorkflowKind.UPPER_BOUND
     else:
+        p = PRECISION_FOR[registers]
         regs = hll_build(ctx, B, p)
         if m == 0:
             cr = (1.0, 1.0, 0.0)

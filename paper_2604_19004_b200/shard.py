@@ -40,6 +40,7 @@ class Shard:
     col_idx: torch.Tensor
     values: torch.Tensor
     report: object = None
+    local: dict = None       # this rank's own counters: rows, nnz_a, products, nnz_c, batches
 
 
 def balanced_cuts(products: np.ndarray, parts: int) -> list:
@@ -110,15 +111,64 @@ def row_products(a_ptr: torch.Tensor, a_col: torch.Tensor, b_ptr: torch.Tensor, 
     return (cum[a_ptr[1:]] - cum[a_ptr[:-1]]).cpu().numpy()
 
 
-def spgemm_sharded(a, b, local_fn, group=None, root=0, device=None, gather=False, products_fn=None):
-    """Row-sharded C = A*B over the ranks of `group`.
+@dataclass
+class ShardPlan:
+    """Everything a step needs, computed once (outside the timed loop):
+    the row cuts, this rank's rows of A, the replicated B, the whole
+    product's workflow decision and this rank's row batches."""
 
-    ``a`` / ``b`` are needed on ``root`` only (host CsrMatrix or DeviceCsr; the
-    other ranks pass None).  ``local_fn(nrows, ncols, row_ptr, col_idx,
-    values, B) -> (row_ptr, col_idx, values, report)`` multiplies this rank's
-    rows.  Returns the local ``Shard``; with ``gather=True`` the root's return
-    value is the full C as a Shard covering all rows.
-    """
+    cuts: list
+    lo: int
+    hi: int
+    A: tuple                 # (nrows, ncols, row_ptr, col_idx, values) of the whole A (broadcast)
+    B: tuple
+    decision: object = None  # engine.Decision of the whole product (root), or None
+    batches: list = None     # row ranges [lo_b, hi_b) covering [lo, hi)
+
+
+_WF = ("symbolic", "estimate", "upper")
+
+
+def _bcast_decision(dec, rank, root, group, device):
+    """Broadcast an engine.Decision (or None) from root as 8 float64s."""
+    t = torch.zeros(8, dtype=torch.float64, device=device)
+    if rank == root and dec is not None:
+        cr = dec.cr if dec.cr is not None else (0.0, 0.0, 0.0)
+        t.copy_(torch.tensor([1.0, float(_WF.index(dec.workflow)), float(dec.registers), float(dec.er),
+                              1.0 if dec.cr is not None else 0.0, cr[0], cr[1], cr[2]], dtype=torch.float64))
+    tot = torch.tensor([dec.total_products if (rank == root and dec is not None) else 0], dtype=torch.int64,
+                       device=device)
+    dist.broadcast(t, src=root, group=group)
+    dist.broadcast(tot, src=root, group=group)
+    v = t.tolist()
+    if v[0] == 0.0:
+        return None
+    from .engine import Decision
+    return Decision(_WF[int(v[1])], int(v[2]), v[3], (v[5], v[6], v[7]) if v[4] else None, int(tot.item()))
+
+
+def row_batches(per: np.ndarray, lo: int, hi: int, budget) -> list:
+    """Contiguous row ranges of [lo, hi) with at most `budget` products each
+    (a single row over budget is its own batch)."""
+    if budget is None or hi <= lo:
+        return [(lo, hi)]
+    out, s, acc = [], lo, 0
+    for r in range(lo, hi):
+        pr = int(per[r - lo])
+        if acc and acc + pr > budget:
+            out.append((s, r))
+            s, acc = r, 0
+        acc += pr
+    out.append((s, hi))
+    return out
+
+
+def plan_shards(a, b, group=None, root=0, device=None, products_fn=None, decide_fn=None,
+                batch_products=None) -> ShardPlan:
+    """Broadcast the operands from `root`, cut A's rows by balanced products,
+    decide the workflow of the whole product once (decide_fn on root, e.g.
+    engine.decide) and split this rank's rows into batches of at most
+    `batch_products` products (C of R-MAT-23 does not fit in HBM at once)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     device = device or torch.device("cpu")
@@ -128,27 +178,116 @@ def spgemm_sharded(a, b, local_fn, group=None, root=0, device=None, gather=False
     same = bool(flag.item())
     B = broadcast_csr(b if rank == root else None, device, root, group)
     A = B if same else broadcast_csr(a if rank == root else None, device, root, group)
-    # balanced cuts computed on the root and broadcast
     cuts_t = torch.empty(world + 1, dtype=torch.int64, device=device)
+    per = None
     if rank == root:
         per = (products_fn or row_products)(A[2], A[3], B[2], B[3], B[1])
         cuts_t.copy_(torch.tensor(balanced_cuts(per, world), dtype=torch.int64))
     dist.broadcast(cuts_t, src=root, group=group)
     cuts = [int(x) for x in cuts_t.tolist()]
+    dec = None
+    if decide_fn is not None:
+        from .device import DeviceCsr
+        d = None
+        if rank == root:
+            Ad = DeviceCsr(A[0], A[1], A[2], A[3], A[4])
+            Bd = Ad if same else DeviceCsr(B[0], B[1], B[2], B[3], B[4])
+            d = decide_fn(Ad, Bd)
+        dec = _bcast_decision(d, rank, root, group, device)
     lo, hi = cuts[rank], cuts[rank + 1]
+    batches = [(lo, hi)]
+    if batch_products is not None and hi > lo:
+        s, e = int(A[2][lo].item()), int(A[2][hi].item())
+        loc = (products_fn or row_products)((A[2][lo:hi + 1] - s).contiguous(), A[3][s:e].contiguous(),
+                                            B[2], B[3], B[1])
+        batches = row_batches(np.asarray(loc), lo, hi, batch_products)
+    return ShardPlan(cuts, lo, hi, A, B, dec, batches)
+
+
+def _rows(A, lo, hi):
     s, e = int(A[2][lo].item()), int(A[2][hi].item())
-    a_rp = (A[2][lo:hi + 1] - s).contiguous()
-    rp, ci, vv, rep = local_fn(hi - lo, A[1], a_rp, A[3][s:e].contiguous(), A[4][s:e].contiguous(), B)
-    # offset exchange: one int64 per rank
-    nnz = torch.tensor([int(ci.numel())], dtype=torch.int64, device=device)
+    return (hi - lo, A[1], (A[2][lo:hi + 1] - s).contiguous(), A[3][s:e].contiguous(), A[4][s:e].contiguous())
+
+
+def _rep_get(rep, k):
+    return rep[k] if isinstance(rep, dict) else getattr(rep, k)
+
+
+def _rep_set(rep, k, v):
+    if isinstance(rep, dict):
+        rep[k] = v
+    else:
+        setattr(rep, k, v)
+
+
+def run_shard(plan: ShardPlan, local_fn, group=None, root=0, gather=False, consume=None):
+    """One row-sharded multiply with a precomputed plan.  Each batch of this
+    rank's rows runs local_fn; ``consume(lo, hi, row_ptr, col_idx, values)``
+    (if given) receives every batch's C and the batch is not kept (C too
+    large for HBM).  Then the offset exchange (all_gather of one int64 per
+    rank) places the shard in the global C, and the report counters that are
+    per-row sums (nnz_c, overflow_row_count, total_products) are summed over
+    ranks so the root's report describes the whole product."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    device = plan.A[2].device
+    kw = {} if plan.decision is None else {"decision": plan.decision}
+    parts, rep, nnz_loc = [], None, 0
+    totals = torch.zeros(3, dtype=torch.int64, device=device)  # nnz_c, overflow rows, products
+    for lo, hi in plan.batches:
+        rp, ci, vv, r = local_fn(*_rows(plan.A, lo, hi), plan.B, **kw)
+        totals += torch.tensor([int(ci.numel()), int(_rep_get(r, "overflow_row_count")),
+                                int(_rep_get(r, "total_products"))], dtype=torch.int64, device=device)
+        rep = r
+        if consume is not None:
+            consume(lo, hi, rp, ci, vv)
+        else:
+            parts.append((rp, ci, vv))
+        nnz_loc += int(ci.numel())
+    if consume is None:
+        if len(parts) == 1:
+            rp, ci, vv = parts[0]
+        else:
+            offs = np.cumsum([0] + [int(p[1].numel()) for p in parts])
+            rp = torch.cat([parts[0][0][:1]] + [p[0][1:] + int(o) for p, o in zip(parts, offs[:-1])])
+            ci = torch.cat([p[1] for p in parts])
+            vv = torch.cat([p[2] for p in parts])
+    else:
+        rp = ci = vv = None
+    nnz = torch.tensor([nnz_loc], dtype=torch.int64, device=device)
     all_nnz = [torch.zeros_like(nnz) for _ in range(world)]
     dist.all_gather(all_nnz, nnz, group=group)
     counts = [int(x.item()) for x in all_nnz]
+    loc_totals = totals.clone()
+    dist.all_reduce(totals, group=group)
+    if rep is not None:
+        nnz_all, ovf_all, prod_all = (int(x) for x in totals.tolist())
+        _rep_set(rep, "nnz_c", nnz_all)
+        _rep_set(rep, "overflow_row_count", ovf_all)
+        _rep_set(rep, "total_products", prod_all)
+        _rep_set(rep, "cr_true", (prod_all / nnz_all) if nnz_all else None)
     offset = int(sum(counts[:rank]))
-    shard = Shard(lo, hi, offset, int(sum(counts)), rp, ci, vv, rep)
-    if not gather:
+    loc = {"rows": plan.hi - plan.lo, "nnz_a": int(plan.A[2][plan.hi].item() - plan.A[2][plan.lo].item()),
+           "products": int(loc_totals[2].item()), "nnz_c": nnz_loc, "batches": len(plan.batches)}
+    shard = Shard(plan.lo, plan.hi, offset, int(sum(counts)), rp, ci, vv, rep, loc)
+    if not gather or consume is not None:
         return shard
-    return gather_shards(shard, counts, cuts, root, group, device)
+    return gather_shards(shard, counts, plan.cuts, root, group, device)
+
+
+def spgemm_sharded(a, b, local_fn, group=None, root=0, device=None, gather=False, products_fn=None,
+                   decide_fn=None):
+    """Row-sharded C = A*B over the ranks of `group`.
+
+    ``a`` / ``b`` are needed on ``root`` only (host CsrMatrix or DeviceCsr; the
+    other ranks pass None).  ``local_fn(nrows, ncols, row_ptr, col_idx,
+    values, B[, decision=...]) -> (row_ptr, col_idx, values, report)``
+    multiplies this rank's rows.  Returns the local ``Shard``; with
+    ``gather=True`` the root's return value is the full C as a Shard covering
+    all rows.  (plan_shards + run_shard, for one call.)
+    """
+    plan = plan_shards(a, b, group, root, device, products_fn, decide_fn)
+    return run_shard(plan, local_fn, group, root, gather)
 
 
 def gather_shards(shard: Shard, counts, cuts, root, group, device):
@@ -217,17 +356,27 @@ def gpu_products_fn(device):
 
 
 def gpu_local_fn(cfg):
-    """local_fn running the single-GPU engine on this rank's device."""
+    """local_fn running the single-GPU engine on this rank's device (with the
+    root's decision for the whole product when the plan carries one)."""
     from .device import DeviceCsr
     from .engine import spgemm
     from dataclasses import replace
 
     cfg = replace(cfg, return_device=True)
 
-    def fn(nrows, ncols_a, row_ptr, col_idx, values, B):
+    def fn(nrows, ncols_a, row_ptr, col_idx, values, B, decision=None):
         Ad = DeviceCsr(nrows, ncols_a, row_ptr, col_idx, values)
         Bd = DeviceCsr(B[0], B[1], B[2], B[3], B[4])
-        c, rep = spgemm(Ad, Bd, cfg)
+        c, rep = spgemm(Ad, Bd, cfg if decision is None else replace(cfg, decision=decision))
         rep.nrows_local = nrows
         return c.row_ptr, c.col_idx, c.values, rep
+    return fn
+
+
+def gpu_decide_fn(cfg, device):
+    """decide_fn for the root: engine.decide on the whole operands."""
+    from .engine import decide
+
+    def fn(A, B):
+        return decide(A, B, cfg, device)
     return fn

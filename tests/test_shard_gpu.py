@@ -35,6 +35,8 @@ def _worker(rank, world, port, case, out_q):
 
 
 def _run(rank, case, out_q):
+    if case.startswith("batched:"):
+        return _run_batched(rank, case.split(":", 1)[1], out_q)
     if True:
         from golden_io import Case
         from paper_2604_19004_b200 import EngineConfig
@@ -78,3 +80,70 @@ def test_gpu_sharded_equals_reference(case):
         row_ptr, col_idx, values = full
     c.check_product(C)
     np.testing.assert_array_equal(full[0][-1:], [c.d["C_ptr"][-1]])
+
+
+def _run_batched(rank, case, out_q):
+    """plan_shards with the root's GPU decision and product-bounded batches;
+    two steps reuse one plan; batches stream through `consume`."""
+    from golden_io import Case
+    from paper_2604_19004_b200 import EngineConfig
+    from paper_2604_19004_b200.device import to_device
+    from paper_2604_19004_b200.shard import gpu_decide_fn, gpu_local_fn, gpu_products_fn, plan_shards, run_shard
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    c = Case(case)
+    a = to_device(c.A, dev) if rank == 0 else None
+    b = to_device(c.B, dev) if rank == 0 else None
+    cfg = EngineConfig()
+    budget = max(1, int(c.d["products"].sum()) // 9)
+    plan = plan_shards(a, b, device=dev, products_fn=gpu_products_fn(dev), decide_fn=gpu_decide_fn(cfg, dev),
+                       batch_products=budget)
+    got = {}
+
+    def consume(lo, hi, rp, ci, vv):
+        got[(lo, hi)] = (rp.cpu().numpy(), ci.cpu().numpy(), vv.cpu().numpy())
+    for _ in range(2):
+        got.clear()
+        sh = run_shard(plan, gpu_local_fn(cfg), consume=consume)
+    r = sh.report
+    out_q.put((rank, len(plan.batches), got, {k: getattr(r, k) for k in
+                                              ("workflow", "registers", "er", "cr_hat", "nnz_c",
+                                               "overflow_row_count", "total_products", "bitmap_query")}))
+
+
+@pytest.mark.parametrize("case", ["corpus1", "enhanced"])
+def test_gpu_sharded_batched_with_global_decision(case):
+    """Config-5 machinery on one GPU (two ranks, gloo): whole-product
+    decision on the root, batches through consume, stitched report equal to
+    the reference's whole-product report, batches equal to the reference C."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from golden_io import Case
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, "batched:" + case, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(2)]
+    errs = [g for g in got if isinstance(g[0], str) and g[0] == "error"]
+    assert not errs, errs[0][2]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    c = Case(case)
+    want = c.meta["reports"]["auto"]
+    cp, cc, cv = c.d["C_ptr"], c.d["C_col"], c.d["C_val"]
+    nb = 0
+    for rank, nbatch, batches, rep in got:
+        nb += nbatch
+        for k in ("workflow", "registers", "nnz_c", "overflow_row_count", "total_products", "bitmap_query"):
+            assert rep[k] == want[k], (rank, k, rep[k], want[k])
+        assert rep["er"] == pytest.approx(want["er"], rel=1e-12)
+        assert rep["cr_hat"] == pytest.approx(want["cr_hat"], rel=1e-12)
+        for (lo, hi), (rp, ci, vv) in batches.items():
+            np.testing.assert_array_equal(rp, cp[lo:hi + 1] - cp[lo])
+            np.testing.assert_array_equal(ci, cc[cp[lo]:cp[hi]])
+            if c.stride == 1:
+                np.testing.assert_allclose(vv, cv[cp[lo]:cp[hi]], rtol=1e-12, atol=0)
+    assert nb > 2

@@ -1,0 +1,14 @@
+#!/bin/bash
+# compute-sanitizer over the small parity cases (tools/sanitize_cases.py):
+# memcheck (out-of-bounds / misaligned / leaks), racecheck (shared-memory
+# hazards), synccheck (illegal barrier use), initcheck (uninitialised global
+# reads).  Logs go to gpurun_out/sanitize_<tool>.txt (summaries in profiles/).
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck initcheck; do
+  extra=""
+  [ "$tool" = "memcheck" ] && extra="--leak-check full"
+  [ "$tool" = "racecheck" ] && extra="--racecheck-report hazard"
+  timeout 3000 compute-sanitizer --tool $tool $extra --print-limit 200 --error-exitcode 9 \
+      python tools/sanitize_cases.py > gpurun_out/sanitize_$tool.txt 2>&1
+  echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|sanitize cases ok' gpurun_out/sanitize_$tool.txt | tr '\n' ' ')"
+done
