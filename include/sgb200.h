@@ -105,15 +105,16 @@ int sg_hll_estimate(int64_t nsel, const int64_t* rows, const int64_t* a_ptr,
  *  win_off  int64[m+1]  window-slot offsets (from sg_window_capacity)
  *  wins     int32[2*win_off[m]] (first column, rank in row) pairs, init -1
  *  nwin     int32[m]    slots used per row, init 0
- *  bm_off   int64[m+1]  word offsets of saved key bitmaps, or NULL
- *  bm_save  uint64[bm_off[m]] saved key bitmaps, or NULL (then the numeric
- *           pass rebuilds each window's key bitmap from the products)
- *  pre_save int32[bm_off[m]] row-relative rank at each saved word (with
- *           bm_save; lets the numeric pass skip the prefix and write C's
- *           columns with a separate streaming expansion)
- * Windows start on 4096-column tiles and hold at most 16384 distinct columns
- * over at most 262144 columns, so a window's bitmap, rank prefix and values
- * sit in shared memory. */
+ *  bm_off   int64[m+1]  64-column word offsets of saved key bitmaps, or NULL
+ *  bm_save  16-byte words [bm_off[m]]: per 64 columns {bits 0-31, row rank
+ *           of bit 0, bits 32-63, row rank of bit 32} (uint32 x 4), or NULL
+ *           (then the numeric pass rebuilds each window's key bitmap from the
+ *           products); lets the numeric pass skip the key pass and the
+ *           prefix, and bulk-copy a window's words into shared memory
+ *  pre_save unused (NULL)
+ * Windows start on 4096-column tiles and hold at most 8192 distinct columns
+ * over at most 131072 columns (greedy cuts in column order), so two windows'
+ * bitmaps and values sit in one SM's shared memory. */
 typedef struct sg_windows {
   const int64_t* win_off;
   int32_t* wins;
@@ -162,18 +163,24 @@ int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t*
                 const sg_windows_t* win, double assist_cr, int64_t skip_max_products, void* ws,
                 size_t ws_bytes, void* stream);
 
-/* Long-row numeric pass over the recorded windows: one CTA (1024 threads)
- * per window, work grouped by column range so concurrent CTAs share B-row
- * slabs in L2; values accumulated in shared memory (fp64) and written sorted
- * at out_off[row] + rank (out_off = row_ptr of C).  With saved bitmaps the
- * columns are written by a separate streaming expansion.  work_buf: 48 bytes
- * x work_cap scratch, work_cap >= total windows. */
+/* Long-row numeric pass over the recorded windows, work grouped by column
+ * range so concurrent CTAs share B-row slabs in L2; values accumulated in
+ * shared memory (fp64) and written sorted at out_off[row] + rank (out_off =
+ * row_ptr of C).  With saved bitmaps: the columns are written by a streaming
+ * expansion, the values by the warp-specialised window kernel (heavy B rows)
+ * and fire-and-forget REDs at the saved ranks (light B rows, < 256 entries);
+ * without: one CTA per window rebuilds the window's keys.  work_buf: scratch
+ * of work_cap >= sg_window_work_bytes(m, nnz(A), total windows) bytes. */
 int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr,
                       const int32_t* a_col, const void* a_val, const int64_t* b_ptr,
                       const int32_t* b_col, const void* b_val, const int64_t* span_lo,
                       const int64_t* span_hi, const sg_windows_t* win, const int64_t* out_off,
                       int32_t* out_col, void* out_val, void* work_buf, int64_t work_cap, void* ws,
                       size_t ws_bytes, void* stream);
+
+/* Scratch bytes sg_window_numeric needs: window work items plus the heavy /
+ * light entry tables of the windowed rows. */
+int64_t sg_window_work_bytes(int64_t m, int64_t nnz_a, int64_t nwindows);
 
 /* Replaces accumulate.plan_rows (accumulate.py:104-181) with the identical
  * integer rules.  pred is int64 (EXACT / UPPER) or f64 (ESTIMATED). */

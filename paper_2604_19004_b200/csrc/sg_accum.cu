@@ -349,7 +349,7 @@ __device__ __forceinline__ void block_row(int64_t row, const int64_t* __restrict
                                           const int32_t* __restrict__ a_col, const V* __restrict__ a_val,
                                           const int64_t* __restrict__ b_ptr, const int32_t* __restrict__ b_col,
                                           const V* __restrict__ b_val, Entries E, int64_t* scan_scratch,
-                                          Op& op, volatile int* stop) {
+                                          Op& op, volatile int* stop, int64_t max_len = NOLIMIT) {
   const int nw = blockDim.x >> 5, w = warp_id();
   const int64_t t1 = a_ptr[row + 1];
   for (int64_t t = a_ptr[row]; t < t1; t += blockDim.x) {
@@ -359,6 +359,7 @@ __device__ __forceinline__ void block_row(int64_t row, const int64_t* __restrict
       const int32_t k = a_col[t + threadIdx.x];
       bs = b_ptr[k];
       len = b_ptr[k + 1] - bs;
+      if (len > max_len) len = 0;  // entry filter (k_win_light: light B rows only)
       if (VALUES) av = (double)a_val[t + threadIdx.x];
     }
     // one scan of (len << 12 | nonempty): segment starts and compacted slots
@@ -1086,8 +1087,8 @@ __device__ __forceinline__ void emit_bits(unsigned long long bits, int32_t colba
 // the window accumulator): a window holds at most WIN_R distinct columns and
 // spans at most WIN_WORDS*64 columns, so its bitmap, rank prefix and values
 // all sit in shared memory.
-constexpr int WIN_WORDS = 4096;  // 262,144 columns
-constexpr int WIN_R = 16384;     // values per window (128 KB fp64)
+constexpr int WIN_WORDS = 2048;  // 131,072 columns
+constexpr int WIN_R = 8192;      // values per window (64 KB fp64: two windows in flight per SM)
 // Windows start on TILE_COLS-column tiles (absolute), so each selected B
 // row's segment in a window is two lookups in the B tile index (no search).
 constexpr int TILE_COLS = 4096;
@@ -1106,7 +1107,7 @@ struct Win {
   int32_t* nwin;
   const int64_t* bm_off;
   unsigned long long* bm_save;
-  int32_t* pre_save;  // row-relative rank at the start of every saved word
+  int32_t* pre_save;  // unused (ranks live in the 16-byte saved words)
   const int64_t* btile_off;
   const int32_t* btile;
 };
@@ -1146,14 +1147,18 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
   Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (NT + 1),
             reinterpret_cast<double*>(ebase) + 2 * (NT + 1)};
   constexpr int64_t WCOLS = (int64_t)BW * 64;
-  __shared__ int64_t last_id;
+  __shared__ int64_t wst_rank, wst_tile;  // open numeric window (count pass)
+  __shared__ int wst_n;                   // windows emitted so far
   for (int64_t b = blockIdx.x; b < nbin; b += gridDim.x) {
     const int64_t row = rows[b];
     const int64_t lo = span_lo[row], hi = span_hi[row];
     const int64_t limit = row_limit(kind, cap, alloc, row);
     int64_t total = 0;
     const int64_t wcap = (MODE == 0 && win_off) ? win_off[row + 1] - win_off[row] : 0;
-    if (threadIdx.x == 0) last_id = -1;
+    if (threadIdx.x == 0) {
+      wst_n = 0;
+      wst_rank = wst_tile = 0;
+    }
     const bool multi = hi - lo + 1 > WCOLS;
     // count-only sweep first when a limit applies and the span needs windows
     bool over = false;
@@ -1208,34 +1213,55 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
         // a window starts at every tile whose id differs from the previous.
         const int64_t gw0 = (wlo - org) >> 6;  // count windows are tile-aligned
         int2* wrow = wins + win_off[row];
-        const int64_t prev_last = last_id;
         if (win.bm_save) {
-          // keep the row's bitmap and word ranks for the numeric windows and
-          // the column expansion (no second key pass, no second prefix)
-          unsigned long long* dst = win.bm_save + win.bm_off[row] + gw0;
-          int32_t* pdst = win.pre_save + win.bm_off[row] + gw0;
+          // keep the row's bitmap with the row rank of every 32-bit half
+          // word, interleaved {lo, rank(lo), hi, rank(hi)} (16 B per 64
+          // columns): the window kernel bulk-copies a window's words into
+          // shared memory as they are (no second key pass, no prefix)
+          uint4* dst = reinterpret_cast<uint4*>(win.bm_save) + win.bm_off[row] + gw0;
           for (int i = threadIdx.x; i < nwords; i += NT) {
-            st_stream(dst + i, bm[i]);
-            st_stream(pdst + i, (int32_t)(total + pre[i]));
+            const unsigned long long wv = bm[i];
+            const uint32_t r = (uint32_t)(total + pre[i]), lo32 = (uint32_t)wv;
+            st_stream_v4(dst + i, make_uint4(lo32, r, (uint32_t)(wv >> 32), r + (uint32_t)__popc(lo32)));
+          }
+        }
+        // windows: greedy cuts over the row's tiles in column order -- a
+        // window takes tiles while it holds <= WIN_R distinct columns over
+        // <= WIN_TILES tiles; warp 0 walks 32 tiles per ballot, one ballot
+        // per cut (the open window carries over to the next sweep)
+        if (warp_id() == 0) {
+          const int lane = lane_id();
+          const int ntiles = (nwords + TILE_WORDS - 1) / TILE_WORDS;
+          const int64_t tg0 = gw0 / TILE_WORDS;
+          int n = wst_n;
+          int64_t rs = wst_rank, ts = wst_tile;
+          for (int ti0 = 0; ti0 < ntiles; ti0 += 32) {
+            const int ti = ti0 + lane;
+            const bool in = ti < ntiles;
+            const int64_t r = in ? total + pre[ti * TILE_WORDS] : 0;
+            const int64_t rn = (ti + 1 < ntiles) ? total + pre[(ti + 1) * TILE_WORDS] : total + wtot;
+            const int64_t tg = tg0 + ti;
+            int from = 0;
+            for (;;) {
+              const bool cut = in && lane >= from &&
+                               (n == 0 || rn - rs > WIN_R || tg - ts + 1 > WIN_TILES);
+              const unsigned m = __ballot_sync(SG_FULL, cut);
+              if (!m) break;
+              const int f = __ffs(m) - 1;
+              if (lane == f && n < wcap) wrow[n] = make_int2((int)(org + (int64_t)TILE_COLS * tg), (int)r);
+              rs = __shfl_sync(SG_FULL, r, f);
+              ts = __shfl_sync(SG_FULL, tg, f);
+              ++n;
+              from = f + 1;
+            }
+          }
+          if (lane == 0) {
+            wst_n = n;
+            wst_rank = rs;
+            wst_tile = ts;
           }
         }
         __syncthreads();
-        const uint32_t tot32 = (uint32_t)total;
-        const int ntiles = (nwords + TILE_WORDS - 1) / TILE_WORDS;
-        for (int ti = threadIdx.x; ti < ntiles; ti += NT) {
-          const uint32_t t = (uint32_t)(gw0 / TILE_WORDS) + (uint32_t)ti;
-          const uint32_t rank = tot32 + (uint32_t)pre[ti * TILE_WORDS];
-          const int64_t id = (int64_t)(rank / (uint32_t)WIN_RP + t / (uint32_t)WIN_TILES);
-          int64_t idp = -1;
-          if (ti > 0) {
-            idp = (int64_t)((tot32 + (uint32_t)pre[(ti - 1) * TILE_WORDS]) / (uint32_t)WIN_RP +
-                            (t - 1) / (uint32_t)WIN_TILES);
-          } else if (t > 0) {
-            idp = prev_last;
-          }
-          if (id != idp && id < wcap) wrow[id] = make_int2((int)(org + (int64_t)TILE_COLS * t), (int)rank);
-          if (ti == ntiles - 1) last_id = id;
-        }
         total += wtot;
         __syncthreads();
         continue;
@@ -1257,7 +1283,7 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
     if (threadIdx.x == 0) {
       if (MODE == 0) {
         counts[row] = total;
-        if (wcap > 0) nwin[row] = (int32_t)(last_id + 1);
+        if (wcap > 0) nwin[row] = (int32_t)min((int64_t)wst_n, wcap);
       } else {
         counts[row] = over ? 0 : total;
         if (overflow) overflow[row] = over ? 1 : 0;
@@ -1413,7 +1439,7 @@ struct WinItem {
   int32_t c0, c1;    // columns [c0, c1); c0 tile-aligned, c1 tile-aligned or row end
   int32_t cnt;       // distinct columns in the window
   int32_t last;      // window ends at the row's end (segment = rest of B row)
-  int32_t pad;
+  int32_t rank0;     // row rank of the window's first column
 };
 
 // B tile index: for B rows with a table, tbl[tbl_off[k] + t] = offset in the
@@ -1509,16 +1535,14 @@ __global__ void __launch_bounds__(NT, CTAS) k_bmr(int64_t nwork, const WinItem* 
     const int cnt = it.cnt;
     const int nwords = (int)(((int64_t)c1 - c0 + 63) >> 6);
     const bool saved = it.bm_word >= 0 && bm_save != nullptr;
+    (void)pre_save;
     if (saved) {
-      // saved 64-bit word i -> interleaved words 2i, 2i+1 with their ranks
-      const unsigned long long* src = bm_save + it.bm_word;
-      const int32_t* psrc = pre_save + it.bm_word;
-      const int r0 = __ldcs(psrc);
+      // saved {lo, rank, hi, rank} words (row ranks) -> window ranks
+      const uint4* src = reinterpret_cast<const uint4*>(bm_save) + it.bm_word;
+      const uint32_t r0 = (uint32_t)it.rank0;
       for (int i = threadIdx.x; i < nwords; i += NT) {
-        const unsigned long long w = __ldcs(src + i);
-        const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
-        const uint32_t p = (uint32_t)(__ldcs(psrc + i) - r0);
-        sts_u4(wp_s + (uint32_t)i * 16, lo, p, hi, p + (uint32_t)__popc(lo));
+        const uint4 q = __ldcs(src + i);
+        sts_u4(wp_s + (uint32_t)i * 16, q.x, q.y - r0, q.z, q.w - r0);
       }
     } else {
       for (int i = threadIdx.x; i < nwords; i += NT) sts_u4(wp_s + (uint32_t)i * 16, 0u, 0u, 0u, 0u);
@@ -1596,6 +1620,486 @@ __global__ void __launch_bounds__(NT, CTAS) k_bmr(int64_t nwork, const WinItem* 
   }
 }
 
+// -------------------------------------------------------------------------
+// KW: warp-specialised window accumulator for long rows with saved bitmaps.
+//
+// One persistent 1024-thread CTA per SM, two windows in flight:
+//   producer warps (KW_PW) take window tickets, bulk-copy the window's saved
+//     {bits, rank} words into one of two bitmap buffers (cp.async.bulk, an
+//     mbarrier counts the bytes), clip every A entry's B row to the window
+//     (B tile index) and publish the non-empty segments in chunks (segment
+//     table {B offset - product start, A value} + a 32-product group table);
+//   consumer warps (KW_CW) take 4-group steps of the current chunk from a
+//     shared counter (no block barrier anywhere), find each product's segment
+//     with one broadcast load + popcount, gather (col, val) from B, rank the
+//     column in the window bitmap and add a*b into the window's fp64 values
+//     in shared memory; the warp that finishes a window last stores its
+//     values (coalesced, streaming) and zeroes them.
+// Chunks (two slots) and windows (two value / bitmap buffers) are handed
+// over with mbarriers, so clipping, bitmap loads and value stores of one
+// window overlap the value pass of the other.  Replaces the
+// setup -> clip -> values -> store phases of k_bmr behind block barriers.
+// Reference: the long-row part of _numeric_phase / _fallback_phase
+// (engine.py:252-328), fallback_accumulate (accumulate.py:274-279).
+
+constexpr int KW_NT = 1024;
+constexpr int KW_PW = 8;                     // producer warps
+constexpr int KW_CW = KW_NT / 32 - KW_PW;    // consumer warps
+constexpr int KW_NP = KW_PW * 32;            // producer threads (one A entry each per batch)
+constexpr int KW_SEG = 512;                  // segments per chunk
+constexpr int KW_GRP = 512;                  // 32-product groups per chunk
+constexpr int KW_PMAX = 32 * KW_GRP;         // products per chunk
+constexpr int KW_U = 4;                      // groups per consumer step
+static_assert(WIN_R * 8 * 2 + WIN_WORDS * 16 * 2 <= 196608, "two windows in shared memory");
+
+enum : int { KW_FIRST = 1, KW_LAST = 2, KW_END = 4 };
+
+struct KwChunk {
+  int64_t d[KW_SEG];       // B position of chunk product p of segment c = d[c] + p
+  double av[KW_SEG];       // A value of segment c
+  int32_t S[KW_SEG + 2];   // chunk-relative first product of segment c
+  int2 grp[KW_GRP];        // group g: {segment of product 32g, segment starts in (32g, 32g+32)}
+  int64_t out_base;        // C index of the window's first entry
+  int32_t P, ng, wslot, flags, c0, cnt, rank0;
+  uint32_t next;           // consumer step counter
+};
+
+struct KwShared {
+  double vals[2][WIN_R];
+  uint4 bm[2][WIN_WORDS];
+  KwChunk ch[2];
+  unsigned long long full[2], empty[2], bm_full[2], win_free[2];
+  int win_done[2];
+  int pscan[KW_PW + 1];
+  int pexcl[KW_NP + 1];
+  int64_t ticket;
+};
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.release.cta.shared::cta.b64 st, [%0]; }" ::"r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1; }" ::"r"(
+                   smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+// wait for the completion of the phase with the given parity (backing off
+// so that waiting warps leave the issue slots to the working ones)
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  const uint32_t a = smem_u32(b);
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void pbar() { asm volatile("bar.sync 1, %0;" ::"n"(KW_NP) : "memory"); }
+__device__ __forceinline__ int pbar_popc(bool p) {
+  int r;
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %1, 0; bar.red.popc.u32 %0, 1, %2, q; }"
+               : "=r"(r)
+               : "r"((unsigned)p), "n"(KW_NP)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
+// Per A entry of a windowed row, resolved once per call instead of once per
+// (entry, window): B row start and length, its tile-index row, the A value.
+// Heavy entries (B rows of >= lh entries) go to k_win, light ones to
+// k_win_light; each list is compacted per row at the row's A offset.
+struct KwEnt {
+  int64_t bs;   // B row start
+  int64_t to;   // B tile index row (-1: none, binary search)
+  double av;    // A value
+  int32_t len;  // B row length
+  int32_t pad;
+};
+
+template <typename V, int NT>
+__global__ void __launch_bounds__(NT) k_win_entries(int64_t m, const int32_t* __restrict__ nwin, Csr A,
+                                                    const int64_t* __restrict__ b_ptr, BTile bt, int lh,
+                                                    KwEnt* __restrict__ hent, int32_t* __restrict__ hcnt,
+                                                    KwEnt* __restrict__ lent, int32_t* __restrict__ lcnt) {
+  __shared__ int64_t scr[NT / 32 + 2];
+  const V* av = (const V*)A.val;
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    if (nwin[row] <= 0) {
+      if (threadIdx.x == 0) hcnt[row] = lcnt[row] = 0;  // no windows: nothing for k_win / k_win_light
+      continue;
+    }
+    const int64_t t0 = A.ptr[row], t1 = A.ptr[row + 1];
+    int64_t nh = 0, nl = 0;
+    for (int64_t t = t0; t < t1; t += NT) {
+      KwEnt e{0, -1, 0.0, 0, 0};
+      int kind = 0;  // 1 heavy, 2 light
+      if (t + threadIdx.x < t1) {
+        const int32_t k = A.col[t + threadIdx.x];
+        e.bs = b_ptr[k];
+        e.len = (int32_t)(b_ptr[k + 1] - e.bs);
+        e.to = bt.off ? bt.off[k] : -1;
+        e.av = (double)av[t + threadIdx.x];
+        kind = e.len >= lh ? 1 : (e.len > 0 ? 2 : 0);
+      }
+      int64_t tot;
+      const int64_t ex = block_excl_scan((int64_t)(kind == 1) | ((int64_t)(kind == 2) << 32), scr, &tot);
+      if (kind == 1) hent[t0 + nh + (ex & 0xffffffffll)] = e;
+      if (kind == 2) lent[t0 + nl + (ex >> 32)] = e;
+      nh += tot & 0xffffffffll;
+      nl += tot >> 32;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      hcnt[row] = (int32_t)nh;
+      lcnt[row] = (int32_t)nl;
+    }
+  }
+}
+
+// a heavy entry's B row clipped to the window [c0, c1): (start, length)
+__device__ __forceinline__ void kw_clip(const KwEnt& en, const int32_t* __restrict__ b_col, BTile bt, int32_t c0,
+                                        int32_t c1, bool last, int64_t& bs, int& len) {
+  const int64_t s = en.bs, e = en.bs + en.len;
+  int64_t ss, ee;
+  if (en.to >= 0) {
+    ss = s + bt.tbl[en.to + c0 / TILE_COLS];
+    ee = last ? e : s + bt.tbl[en.to + c1 / TILE_COLS];
+  } else {
+    ss = lower_bound_col(b_col, s, e, c0);
+    ee = last ? e : lower_bound_col(b_col, ss, e, c1);
+  }
+  bs = ss;
+  len = (int)(ee - ss);
+}
+
+template <typename V>
+__device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const WinItem* __restrict__ work,
+                                            const Csr& A, const Csr& B, const BTile& bt,
+                                            const uint4* __restrict__ bm16, const KwEnt* __restrict__ hent,
+                                            unsigned long long* ticket) {
+  const int tid = threadIdx.x;  // 0 .. KW_NP-1
+  const int lane = lane_id(), pw = warp_id();
+  unsigned wseq = 0, cseq = 0;
+  int nprod = 0, nseg = 0;
+  KwChunk* ch = nullptr;
+
+  auto acquire = [&]() {
+    const unsigned cs = cseq & 1u;
+    mbar_wait(&sh.empty[cs], ((cseq >> 1) & 1u) ^ 1u);
+    ch = &sh.ch[cs];
+    nprod = nseg = 0;
+  };
+  auto publish = [&](int flags, const WinItem& it, unsigned wslot) {
+    // group table of the chunk: owner of every group's first product and
+    // the segment starts inside the group (S strictly increasing)
+    const int ng = (nprod + 31) >> 5;
+    if (tid == 0) ch->S[nseg] = nprod;
+    pbar();
+    for (int g = tid; g < ng; g += KW_NP) {
+      const int q = 32 * g;
+      int lo = 0, hi = nseg - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ch->S[mid] <= q) lo = mid; else hi = mid - 1;
+      }
+      unsigned mask = 0;
+      for (int c = lo + 1; c < nseg; ++c) {
+        const int dd = ch->S[c] - q;
+        if (dd >= 32) break;
+        mask |= 1u << dd;
+      }
+      ch->grp[g] = make_int2(lo, (int)mask);
+    }
+    if (tid == 0) {
+      ch->P = nprod;
+      ch->ng = ng;
+      ch->wslot = (int)wslot;
+      ch->flags = flags;
+      ch->c0 = it.c0;
+      ch->cnt = it.cnt;
+      ch->rank0 = it.rank0;
+      ch->out_base = it.out_base;
+      ch->next = 0;
+    }
+    pbar();
+    if (tid == 0) mbar_arrive(&sh.full[cseq & 1u]);
+    ++cseq;
+  };
+
+  for (;;) {
+    if (tid == 0) sh.ticket = (int64_t)atomicAdd(ticket, 1ull);
+    pbar();
+    const int64_t b = sh.ticket;
+    pbar();
+    if (b >= nwork) break;
+    const WinItem it = work[b];
+    const unsigned wslot = wseq & 1u;
+    // the window buffers are free once the window two back was stored
+    mbar_wait(&sh.win_free[wslot], ((wseq >> 1) & 1u) ^ 1u);
+    if (tid == 0) {
+      const unsigned nwords = (unsigned)(((int64_t)it.c1 - it.c0 + 63) >> 6);
+      mbar_arrive_tx(&sh.bm_full[wslot], nwords * 16u);
+      bulk_g2s(&sh.bm[wslot][0], bm16 + it.bm_word, nwords * 16u, &sh.bm_full[wslot]);
+    }
+    acquire();
+    int flags = KW_FIRST;
+    const int64_t t0 = it.t0, t1 = it.t0 + it.t_len;
+    for (int64_t tb = t0; tb < t1; tb += KW_NP) {
+      const int64_t t = tb + tid;
+      int64_t bs = 0;
+      int len = 0;
+      double a = 0.0;
+      if (t < t1) {
+        const KwEnt en = hent[t];
+        kw_clip(en, B.col, bt, it.c0, it.c1, it.last != 0, bs, len);
+        a = en.av;
+      }
+      // batch scan of (len << 9 | non-empty)
+      const int pk = (len << 9) | (len > 0 ? 1 : 0);
+      const int inc = warp_incl_scan(pk);
+      if (lane == 31) sh.pscan[pw] = inc;
+      pbar();
+      int wbase = 0;
+      for (int w = 0; w < pw; ++w) wbase += sh.pscan[w];
+      const int excl = wbase + inc - pk;
+      sh.pexcl[tid] = excl;
+      if (tid == KW_NP - 1) sh.pexcl[KW_NP] = excl + pk;
+      pbar();
+      int from = 0;
+      while (from < KW_NP) {
+        const int base = sh.pexcl[from];
+        const int rel_in = excl + pk - base;  // inclusive, relative to `from`
+        const bool fits = tid >= from && nprod + (rel_in >> 9) <= KW_PMAX && nseg + (rel_in & 511) <= KW_SEG;
+        const int nfit = pbar_popc(fits);
+        if (fits && len > 0) {
+          const int rel_ex = excl - base;
+          const int c = nseg + (rel_ex & 511);
+          const int S = nprod + (rel_ex >> 9);
+          ch->S[c] = S;
+          ch->d[c] = bs - S;
+          ch->av[c] = a;
+        }
+        const int tot = sh.pexcl[from + nfit] - base;
+        nprod += tot >> 9;
+        nseg += tot & 511;
+        from += nfit;
+        if (from < KW_NP) {  // chunk full: publish it, continue in the next slot
+          publish(flags, it, wslot);
+          flags = 0;
+          acquire();
+        }
+      }
+      pbar();  // pexcl / pscan reuse
+    }
+    publish(flags | KW_LAST, it, wslot);
+    ++wseq;
+  }
+  acquire();
+  nprod = nseg = 0;
+  WinItem none{};
+  publish(KW_END, none, 0);
+}
+
+template <typename V>
+__device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, V* __restrict__ out_val) {
+  const int lane = lane_id();
+  const unsigned le = lanemask_le();
+  const int32_t* __restrict__ b_col = B.col;
+  const V* __restrict__ b_val = (const V*)B.val;
+  unsigned cseq = 0;
+  unsigned wuse[2] = {0u, 0u};
+  for (;;) {
+    const unsigned cs = cseq & 1u;
+    mbar_wait(&sh.full[cs], (cseq >> 1) & 1u);
+    KwChunk& ch = sh.ch[cs];
+    const int flags = ch.flags;
+    if (flags & KW_END) break;
+    const int ng = ch.ng, P = ch.P, ws = ch.wslot, c0 = ch.c0, cnt = ch.cnt, rank0 = ch.rank0;
+    const int64_t out_base = ch.out_base;
+    if (flags & KW_FIRST) {
+      mbar_wait(&sh.bm_full[ws], wuse[ws] & 1u);
+      ++wuse[ws];
+    }
+    WinAddOp op{smem_u32(&sh.bm[ws][0]), smem_u32(&sh.vals[ws][0]) - (uint32_t)rank0 * 8u, c0};
+    const uint32_t grp_s = smem_u32(&ch.grp[0]), d_s = smem_u32(&ch.d[0]), av_s = smem_u32(&ch.av[0]);
+    for (;;) {
+      unsigned g0 = 0;
+      if (lane == 0) g0 = atomicAdd(&ch.next, (unsigned)KW_U);
+      g0 = __shfl_sync(SG_FULL, g0, 0);
+      if ((int)g0 >= ng) break;
+      int32_t col[KW_U];
+      double v[KW_U];
+      if (((int)g0 + KW_U) * 32 <= P) {
+#pragma unroll
+        for (int u = 0; u < KW_U; ++u) {
+          const uint2 gr = lds_v2u32(grp_s + (g0 + u) * 8u);
+          const uint32_t c = gr.x + (uint32_t)__popc(gr.y & le);
+          const int64_t pos = lds_s64(d_s + c * 8u) + (int64_t)(((int)g0 + u) * 32 + lane);
+          col[u] = __ldg(b_col + pos);
+          v[u] = lds_f64(av_s + c * 8u) * (double)__ldg(b_val + pos);
+        }
+#pragma unroll
+        for (int u = 0; u < KW_U; ++u) op(col[u], v[u]);
+      } else {
+        bool ok[KW_U];
+#pragma unroll
+        for (int u = 0; u < KW_U; ++u) {
+          const int p = ((int)g0 + u) * 32 + lane;
+          ok[u] = p < P;
+          col[u] = 0;
+          v[u] = 0.0;
+          if (ok[u]) {
+            const uint2 gr = lds_v2u32(grp_s + (g0 + u) * 8u);
+            const uint32_t c = gr.x + (uint32_t)__popc(gr.y & le);
+            const int64_t pos = lds_s64(d_s + c * 8u) + (int64_t)p;
+            col[u] = __ldg(b_col + pos);
+            v[u] = lds_f64(av_s + c * 8u) * (double)__ldg(b_val + pos);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < KW_U; ++u)
+          if (ok[u]) op(col[u], v[u]);
+      }
+    }
+    __syncwarp();
+    if (flags & KW_LAST) __threadfence_block();
+    if (lane == 0) mbar_arrive(&sh.empty[cs]);
+    if (flags & KW_LAST) {
+      int n = 0;
+      if (lane == 0) n = atomicAdd(&sh.win_done[ws], 1);
+      n = __shfl_sync(SG_FULL, n, 0);
+      if (n == KW_CW - 1) {
+        // last warp out: store the window's values (coalesced, streaming)
+        // and zero them for the window after next
+        const uint32_t vs = smem_u32(&sh.vals[ws][0]);
+        V* dst = out_val + out_base;
+        int i = lane;
+        for (; i + 96 < cnt; i += 128) {
+          const double x0 = lds_f64(vs + i * 8u), x1 = lds_f64(vs + (i + 32) * 8u);
+          const double x2 = lds_f64(vs + (i + 64) * 8u), x3 = lds_f64(vs + (i + 96) * 8u);
+          st_stream(dst + i, (V)x0);
+          st_stream(dst + i + 32, (V)x1);
+          st_stream(dst + i + 64, (V)x2);
+          st_stream(dst + i + 96, (V)x3);
+          sts_f64(vs + i * 8u, 0.0);
+          sts_f64(vs + (i + 32) * 8u, 0.0);
+          sts_f64(vs + (i + 64) * 8u, 0.0);
+          sts_f64(vs + (i + 96) * 8u, 0.0);
+        }
+        for (; i < cnt; i += 32) {
+          st_stream(dst + i, (V)lds_f64(vs + i * 8u));
+          sts_f64(vs + i * 8u, 0.0);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          sh.win_done[ws] = 0;
+          mbar_arrive(&sh.win_free[ws]);
+        }
+      }
+    }
+    ++cseq;
+  }
+}
+
+// Light entries of the windowed rows: products of B rows shorter than lh
+// (which k_win skips) are added straight into C's values with fire-and-forget
+// fp64 REDs at the column's row rank, read from the row's saved bitmap (L2).
+// R-MAT-20: B rows < 256 carry 4.4% of the long-row products but 57% of the
+// long rows' A entries, i.e. of the window kernel's clipping work.
+template <typename V>
+struct LightOp {
+  const uint2* bm;  // the row's saved {bits, rank} pairs, one per 32 columns
+  int32_t org;      // column of the row's first saved bit
+  V* out;           // C values of the row
+  __device__ __forceinline__ void operator()(int32_t col, double v) {
+    const uint32_t x = (uint32_t)(col - org);
+    const uint2 p = __ldg(bm + (x >> 5));
+    gmem_red(out + (p.y + __popc(p.x & ((2u << (x & 31)) - 1u)) - 1u), (V)v);
+  }
+};
+
+template <typename V, int NT>
+__global__ void __launch_bounds__(NT) k_win_light(int64_t m, const int32_t* __restrict__ lcnt, Csr A, Csr B,
+                                                  const int64_t* __restrict__ span_lo,
+                                                  const int64_t* __restrict__ bm_off, const uint4* __restrict__ bm16,
+                                                  const int64_t* __restrict__ row_ptr,
+                                                  const KwEnt* __restrict__ lent, V* __restrict__ out_val) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int64_t scr[NT / 32 + 2];
+  Entries E{reinterpret_cast<int64_t*>(smem), reinterpret_cast<int64_t*>(smem) + (NT + 1),
+            reinterpret_cast<double*>(smem) + 2 * (NT + 1)};
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    const int n = lcnt[row];
+    if (n <= 0) continue;
+    LightOp<V> op{reinterpret_cast<const uint2*>(bm16 + bm_off[row]), (int32_t)win_origin(span_lo[row]),
+                  out_val + row_ptr[row]};
+    const KwEnt* le = lent + A.ptr[row];
+    for (int j0 = 0; j0 < n; j0 += NT) {
+      int64_t bs = 0, len = 0;
+      double av = 0.0;
+      if (j0 + (int)threadIdx.x < n) {
+        const KwEnt en = le[j0 + threadIdx.x];
+        bs = en.bs;
+        len = en.len;
+        av = en.av;
+      }
+      int64_t tot;
+      const int64_t ex = block_excl_scan((len << 12) | (int64_t)(len > 0), scr, &tot);
+      const int64_t S = ex >> 12, pos = ex & 4095;
+      if (len > 0) {
+        E.S[pos] = S;
+        E.d[pos] = bs - S;
+        E.av[pos] = av;
+      }
+      __syncthreads();
+      block_products<true, V>(E, (int)(tot & 4095), tot >> 12, B.col, (const V*)B.val, op);
+    }
+  }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* __restrict__ work, Csr A, Csr B,
+                                                  BTile bt, const uint4* __restrict__ bm16,
+                                                  const KwEnt* __restrict__ hent, V* __restrict__ out_val,
+                                                  unsigned long long* __restrict__ ticket) {
+  extern __shared__ __align__(128) unsigned char kw_smem[];
+  KwShared& sh = *reinterpret_cast<KwShared*>(kw_smem);
+  for (int i = threadIdx.x; i < 2 * WIN_R; i += KW_NT) (&sh.vals[0][0])[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&sh.full[j], 1);
+      mbar_init(&sh.empty[j], KW_CW);
+      mbar_init(&sh.bm_full[j], 1);
+      mbar_init(&sh.win_free[j], 1);
+      sh.win_done[j] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp_id() < KW_PW)
+    kw_producer<V>(sh, nwork, work, A, B, bt, bm16, hent, ticket);
+  else
+    kw_consumer<V>(sh, B, out_val);
+}
+
 // Column expansion of the long rows from the saved key bitmaps:
 // C.col_idx[row_ptr[row] + rank ..] for every set bit, ascending.  Blocks
 // sweep the window work items (each <= WIN_WORDS words, so the work is even).
@@ -1623,7 +2127,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT) k_expand_scan(int64_t nwork, co
     const WinItem it = work[b];
     if (it.bm_word < 0) continue;
     const int64_t nw = ((int64_t)it.c1 - it.c0 + 63) >> 6;
-    const unsigned long long* bm = bm_save + it.bm_word;
+    const uint4* bm = reinterpret_cast<const uint4*>(bm_save) + it.bm_word;
     int32_t* out = out_col + it.out_base;
     int carry = 0;
     for (int64_t i0 = 0; i0 < nw; i0 += U * NT) {
@@ -1632,7 +2136,12 @@ __global__ void __launch_bounds__(NT, 2048 / NT) k_expand_scan(int64_t nwork, co
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t i = i0 + u * NT + threadIdx.x;
-        bits[u] = i < nw ? __ldcs(bm + i) : 0ull;
+        if (i < nw) {
+          const uint4 q = __ldcs(bm + i);
+          bits[u] = ((unsigned long long)q.z << 32) | q.x;
+        } else {
+          bits[u] = 0ull;
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1689,6 +2198,69 @@ __global__ void __launch_bounds__(NT, 2048 / NT) k_expand_scan(int64_t nwork, co
   }
 }
 
+// Column expansion from the saved 16-byte words, whose stored row ranks give
+// every word's output position directly: no scan and no rank barrier; the
+// step's columns are staged in shared memory (double-buffered, shifted by the
+// output's misalignment) and leave as aligned 16-byte stores, so a step costs
+// one block barrier.
+template <int NT, int U, int CAP>
+__global__ void __launch_bounds__(NT) k_expand_rank(int64_t nwork, const WinItem* __restrict__ work,
+                                                    const uint4* __restrict__ bm16, int32_t* __restrict__ out_col) {
+  static_assert(CAP % 4 == 0, "16-byte staging passes");
+  __shared__ __align__(16) int sbuf[2][CAP];
+  int par = 0;
+  for (int64_t b = blockIdx.x; b < nwork; b += gridDim.x) {
+    const WinItem it = work[b];
+    if (it.bm_word < 0) continue;
+    const int64_t nw = ((int64_t)it.c1 - it.c0 + 63) >> 6;
+    const uint4* bm = bm16 + it.bm_word;
+    int32_t* out = out_col + it.out_base;
+    const uint32_t r0 = (uint32_t)it.rank0;
+    for (int64_t i0 = 0; i0 < nw; i0 += U * NT) {
+      uint4 q[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * NT + threadIdx.x;
+        q[u] = i < nw ? __ldcs(bm + i) : make_uint4(0u, 0u, 0u, 0u);
+      }
+      const uint32_t sb = (i0 == 0 ? r0 : __ldg(&bm[i0].y)) - r0;  // step base (window-relative)
+      const uint32_t se = (i0 + U * NT < nw ? __ldg(&bm[i0 + U * NT].y) - r0 : (uint32_t)it.cnt);
+      const int total = (int)(se - sb);
+      int32_t* o = out + sb;
+      const int mis = (int)(((uintptr_t)o & 15) >> 2);
+      const int end = mis + total;
+      const bool staged = end <= CAP;
+      int* buf = sbuf[par];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * NT + threadIdx.x;
+        if (i < nw && (q[u].x | q[u].z)) {
+          const int32_t cb = it.c0 + (int32_t)(64 * i);
+          const int p0 = (int)(q[u].y - r0 - sb);
+          emit_bits(((unsigned long long)q[u].z << 32) | q[u].x, cb, staged ? buf + mis + p0 : o + p0);
+        }
+      }
+      if (staged) {
+        __syncthreads();
+        int32_t* oa = o - mis;
+        for (int k = threadIdx.x; k < (end + 3) >> 2; k += NT) {
+          const int4 v = reinterpret_cast<const int4*>(buf)[k];
+          const int e0 = 4 * k;
+          if (e0 >= mis && e0 + 4 <= end) {
+            reinterpret_cast<int4*>(oa)[k] = v;
+          } else {
+            if (e0 >= mis) oa[e0] = v.x;
+            if (e0 + 1 >= mis && e0 + 1 < end) oa[e0 + 1] = v.y;
+            if (e0 + 2 >= mis && e0 + 2 < end) oa[e0 + 2] = v.z;
+            if (e0 + 3 >= mis && e0 + 3 < end) oa[e0 + 3] = v.w;
+          }
+        }
+        par ^= 1;  // the next step stages into the other buffer
+      }
+    }
+  }
+}
+
 // Work items: one per used window, grouped into NBUCKET column-range buckets
 // (bucket = c0 * NBUCKET / ncols) so the dynamic ticket order sweeps B's
 // columns once.
@@ -1737,8 +2309,8 @@ __global__ void k_win_scatter(int64_t m, int64_t ncols, const int64_t* __restric
                               const int64_t* __restrict__ span_lo, const int64_t* __restrict__ span_hi,
                               const int64_t* __restrict__ win_off, const int2* __restrict__ wins,
                               const int32_t* __restrict__ nwin, const int64_t* __restrict__ out_off,
-                              const int64_t* __restrict__ bm_off, unsigned long long* __restrict__ cursor,
-                              WinItem* __restrict__ work) {
+                              const int64_t* __restrict__ bm_off, const int32_t* __restrict__ heavy_cnt,
+                              unsigned long long* __restrict__ cursor, WinItem* __restrict__ work) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int n = nwin[i];
@@ -1753,9 +2325,10 @@ __global__ void k_win_scatter(int64_t m, int64_t ncols, const int64_t* __restric
                     it.cnt = (int32_t)cnt;
                     it.out_base = out_off[i] + rank0;
                     it.t0 = a_ptr[i];
-                    it.t_len = (int32_t)(a_ptr[i + 1] - a_ptr[i]);
+                    // k_win walks the row's heavy entry table (same A offset)
+                    it.t_len = heavy_cnt ? heavy_cnt[i] : (int32_t)(a_ptr[i + 1] - a_ptr[i]);
                     it.bm_word = bm_off ? bm_off[i] + ((int64_t)c0 - org) / 64 : -1;
-                    it.pad = 0;
+                    it.rank0 = rank0;
                     const unsigned long long slot =
                         atomicAdd(&cursor[win_class(cnt, c0, c1) * NBUCKET + win_bucket(c0, ncols)], 1ull);
                     work[slot] = it;
@@ -2170,11 +2743,76 @@ static int launch_bmr(int64_t n, const WinItem* work, const Csr& A, const Csr& B
   return check_cuda("k_bmr");
 }
 
+// B rows shorter than this go through k_win_light (0: every entry in k_win)
+static int light_len() {
+  static int v = [] {
+    const char* e = getenv("SG_LIGHT_LEN");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+
+// window scratch: WinItems, then the heavy and light entry tables (indexed by
+// A position) and their per-row counts
+struct WinScratch {
+  WinItem* work;
+  KwEnt* hent;
+  KwEnt* lent;
+  int32_t* hcnt;
+  int32_t* lcnt;
+};
+static size_t win_scratch_bytes(int64_t m, int64_t nnz_a, int64_t nwin) {
+  return align256((size_t)nwin * sizeof(WinItem)) + 2 * align256((size_t)nnz_a * sizeof(KwEnt)) +
+         2 * align256((size_t)m * 4) + 256;
+}
+static WinScratch win_scratch(void* buf, int64_t m, int64_t nnz_a, int64_t nwin) {
+  unsigned char* p = reinterpret_cast<unsigned char*>(((uintptr_t)buf + 255) & ~(uintptr_t)255);
+  WinScratch w;
+  w.work = reinterpret_cast<WinItem*>(p);
+  p += align256((size_t)nwin * sizeof(WinItem));
+  w.hent = reinterpret_cast<KwEnt*>(p);
+  p += align256((size_t)nnz_a * sizeof(KwEnt));
+  w.lent = reinterpret_cast<KwEnt*>(p);
+  p += align256((size_t)nnz_a * sizeof(KwEnt));
+  w.hcnt = reinterpret_cast<int32_t*>(p);
+  p += align256((size_t)m * 4);
+  w.lcnt = reinterpret_cast<int32_t*>(p);
+  return w;
+}
+
+template <typename V>
+static int launch_kwin(int64_t n, const WinItem* work, const Csr& A, const Csr& B, const BTile& bt, const Win& W,
+                       const KwEnt* hent, void* out_val, unsigned long long* ticket, cudaStream_t s) {
+  constexpr size_t sm = sizeof(KwShared);
+  auto kern = k_win<V>;
+  if (int rc = set_smem(kern, sm)) return rc;
+  const int grid = (int)std::min<int64_t>(n, (int64_t)num_sms());
+  kern<<<grid, KW_NT, sm, s>>>(n, work, A, B, bt, reinterpret_cast<const uint4*>(W.bm_save), hent, (V*)out_val,
+                               ticket);
+  return check_cuda("k_win");
+}
+
+template <typename V>
+static int launch_light(int64_t m, const Csr& A, const Csr& B, const Win& W, const int64_t* span_lo,
+                        const int64_t* row_ptr, const WinScratch& ws, void* out_val, cudaStream_t s) {
+  constexpr int NT = 256;
+  constexpr size_t sm = (size_t)3 * (NT + 1) * 8;
+  auto kern = k_win_light<V, NT>;
+  if (int rc = set_smem(kern, sm)) return rc;
+  const int grid = (int)std::min<int64_t>(m, (int64_t)num_sms() * 8);
+  ktimer_begin("k_win_light", s);
+  kern<<<grid, NT, sm, s>>>(m, ws.lcnt, A, B, span_lo, W.bm_off, reinterpret_cast<const uint4*>(W.bm_save), row_ptr,
+                            ws.lent, (V*)out_val);
+  ktimer_end(s);
+  return check_cuda("k_win_light");
+}
+
 extern "C" {
 
 static Win to_win(const sg_windows_t* w) {
   if (!w) return Win{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  const bool sv = w->bm_save != nullptr && w->pre_save != nullptr;
+  const bool sv = w->bm_save != nullptr;  // 16-byte {lo, rank, hi, rank} words (pre_save unused)
   return Win{w->win_off, reinterpret_cast<int2*>(w->wins), w->nwin, w->bm_off,
              sv ? reinterpret_cast<unsigned long long*>(w->bm_save) : nullptr, sv ? w->pre_save : nullptr,
              w->btile_off, w->btile};
@@ -2330,29 +2968,58 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
     if (c == 1) nsmall = nwork;
   }
   if (nwork == 0) return SG_OK;
-  if (nwork > work_cap) {
-    set_error("sg_window_numeric: work buffer too small");
+  int64_t nnz_a = 0;
+  cudaMemcpyAsync(&nnz_a, a_ptr + m, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric nnz", 0);
+  if (win_scratch_bytes(m, nnz_a, nwork) > (size_t)work_cap) {
+    set_error("sg_window_numeric: work buffer too small (sg_window_work_bytes)");
     return SG_ERR_WORKSPACE;
   }
+  const WinScratch wsc = win_scratch(work_buf, m, nnz_a, nwork);
+  WinItem* work = wsc.work;
+  const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
+  const BTile bt{W.btile_off, W.btile};
+  const int lh = W.bm_save ? light_len() : 0;
+  if (W.bm_save) {
+    // heavy / light entry tables of the windowed rows (k_win, k_win_light)
+    auto ek = dtype == SG_F64 ? k_win_entries<double, 256> : k_win_entries<float, 256>;
+    ek<<<(int)std::min<int64_t>(m, (int64_t)num_sms() * 16), 256, 0, s>>>(m, W.nwin, A, b_ptr, bt, lh, wsc.hent,
+                                                                           wsc.hcnt, wsc.lent, wsc.lcnt);
+    if (int rc = check_cuda("k_win_entries")) return rc;
+  }
   cudaMemcpyAsync(cnt, cur, sizeof(cur), cudaMemcpyHostToDevice, s);
-  WinItem* work = reinterpret_cast<WinItem*>(work_buf);
   k_win_scatter<<<grid_for(m, 256), 256, 0, s>>>(m, b_ncols, a_ptr, span_lo, span_hi, W.off, W.wins, W.nwin,
-                                                 out_off, W.bm_save ? W.bm_off : nullptr, cnt, work);
+                                                 out_off, W.bm_save ? W.bm_off : nullptr,
+                                                 W.bm_save ? wsc.hcnt : nullptr, cnt, work);
   if (int rc = check_cuda("k_win_scatter")) return rc;
   if (W.bm_save) {
     ktimer_begin("k_expand", s);
-    k_expand_scan<EXP_NT, 4, 6144><<<(int)std::min<int64_t>(nwork, (int64_t)num_sms() * (2048 / EXP_NT)), EXP_NT,
-                                      0, s>>>(nwork, work, W.bm_save, out_col);
+    k_expand_rank<EXP_NT, 4, 6144><<<(int)std::min<int64_t>(nwork, (int64_t)num_sms() * 4), EXP_NT, 0, s>>>(
+        nwork, work, reinterpret_cast<const uint4*>(W.bm_save), out_col);
     ktimer_end(s);
     if (int rc = check_cuda("k_expand")) return rc;
   }
   // tickets live after the cursors (the host copy above must finish first)
   unsigned long long* tickets = cnt + 2 * NBUCKET;
   cudaMemsetAsync(tickets, 0, 2 * sizeof(unsigned long long), s);
-  const Csr A{a_ptr, a_col, a_val}, B{b_ptr, b_col, b_val};
-  const BTile bt{W.btile_off, W.btile};
   ktimer_begin("k_bmr", s);
-  if (nsmall > 0) {
+  if (W.bm_save) {
+    // saved bitmaps: the warp-specialised window kernel takes every window
+    // (both size classes, in ticket order), heavy entries only
+    int rc = dtype == SG_F64 ? launch_kwin<double>(nwork, work, A, B, bt, W, wsc.hent, out_val, tickets, s)
+                             : launch_kwin<float>(nwork, work, A, B, bt, W, wsc.hent, out_val, tickets, s);
+    if (rc) return rc;
+    ktimer_end(s);
+    // then the light entries add on top of the stored window values
+    if (lh > 1) {
+      rc = dtype == SG_F64 ? launch_light<double>(m, A, B, W, span_lo, out_off, wsc, out_val, s)
+                           : launch_light<float>(m, A, B, W, span_lo, out_off, wsc, out_val, s);
+      if (rc) return rc;
+    }
+    if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric end", 0);
+    return SG_OK;
+  }
+  if (nsmall > 0 && !W.bm_save) {
     int rc = dtype == SG_F64
                  ? launch_bmr<double, SMALL_NT, SMALL_WORDS, SMALL_R, 2>(nsmall, work, A, B, bt, W, out_col, out_val,
                                                                            tickets, s)
@@ -2371,6 +3038,10 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   // `cur` (host) is read by the async copy above: keep it alive until done
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric end", 0);
   return SG_OK;
+}
+
+int64_t sg_window_work_bytes(int64_t m, int64_t nnz_a, int64_t nwindows) {
+  return (int64_t)win_scratch_bytes(m, nnz_a, nwindows);
 }
 
 int sg_btile_plan(int64_t k, int64_t b_ncols, const int64_t* b_ptr, int64_t budget_bytes, int64_t* tbl_scan,

@@ -108,6 +108,7 @@ __device__ __forceinline__ void st_stream(int32_t* p, int32_t v) { __stcs(p, v);
 __device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(float* p, float v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(unsigned long long* p, unsigned long long v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream_v4(uint4* p, uint4 v) { __stcs(p, v); }
 
 __device__ __forceinline__ uint32_t next_pow2_u32(uint32_t x) {
   return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));

@@ -187,7 +187,7 @@ class Windows:
         s.win_off, s.wins, s.nwin = ptr(self.off), ptr(self.wins), ptr(self.nwin)
         s.bm_off = ptr(self.bm_off) if self.bm_save is not None else None
         s.bm_save = ptr(self.bm_save) if self.bm_save is not None else None
-        s.pre_save = ptr(self.pre_save) if self.bm_save is not None else None
+        s.pre_save = None  # ranks live in the 16-byte saved words
         s.btile_off = ptr(self.btile_off)
         s.btile = ptr(self.btile)
         self._struct = s  # keep alive for the call
@@ -227,10 +227,8 @@ def windows(ctx: _Ctx, m, products, lo, hi, select) -> Windows:
         # cudaMemGetInfo, which costs milliseconds under expandable segments
         free = _device_total(ctx.device) - torch.cuda.memory_allocated(ctx.device)
         free += _ARENA.held_bytes(ctx.device)
-        if 12 * words <= BITMAP_SAVE_SHARE * free:
-            got = _ARENA.take(ctx, words)
-            if got is not None:
-                bm_save, pre_save = got
+        if 16 * words <= BITMAP_SAVE_SHARE * free:
+            bm_save = _ARENA.take(ctx, words)
     return Windows(off, wins, nwin, bm_off, bm_save, pre_save, total)
 
 
@@ -264,7 +262,7 @@ class _BitmapArena:
     def held_bytes(self, device) -> int:
         with self.lock:
             b = self.bufs.get(str(device))
-        return 0 if b is None else b[0].numel() * 12
+        return 0 if b is None else b.numel() * 8
 
     def take(self, ctx, words):
         key = str(ctx.device)
@@ -273,18 +271,16 @@ class _BitmapArena:
             cur = None if shared else self.bufs.get(key)
             if not shared:
                 self.busy.add(key)
-                if cur is not None and cur[0].numel() < words:
+                if cur is not None and cur.numel() < 2 * words:
                     del self.bufs[key]  # too small: replace
                     cur = None
         if cur is None:
             n = words if shared else int(words * self.HEADROOM)
             try:
-                cur = (torch.empty(n, dtype=torch.int64, device=ctx.device),
-                       torch.empty(n, dtype=torch.int32, device=ctx.device))
+                cur = torch.empty(2 * n, dtype=torch.int64, device=ctx.device)  # 16 B per word
             except torch.OutOfMemoryError:
                 try:
-                    cur = (torch.empty(words, dtype=torch.int64, device=ctx.device),
-                           torch.empty(words, dtype=torch.int32, device=ctx.device))
+                    cur = torch.empty(2 * words, dtype=torch.int64, device=ctx.device)
                 except torch.OutOfMemoryError:
                     if not shared:
                         self.release(ctx.device)
@@ -294,7 +290,7 @@ class _BitmapArena:
                     self.bufs[key] = cur
         if not shared:
             ctx.arena_taken = True
-        return cur[0][:words], cur[1][:words]
+        return cur[:2 * words]
 
     def release(self, device):
         with self.lock:
@@ -665,10 +661,11 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         C_col, C_val = alloc_c(ctx, nnz_c, dtype, win)
     if win is not None and win.total:
         btile(ctx, B, win)
-        work = ctx.empty(6 * win.total, torch.int64)  # one 48-byte item per window
+        wbytes = int(_lib.load().sg_window_work_bytes(m, A.nnz, win.total))
+        work = ctx.empty((wbytes + 7) // 8, torch.int64)  # window items + entry tables
         ws, wsb = ctx.workspace(max(m, 1))
         _lib.call("sg_window_numeric", m, n, dcode, *Aargs, ptr(span_lo), ptr(span_hi), win.struct(),
-                  ptr(row_ptr), ptr(C_col), ptr(C_val), ptr(work), win.total, ws, wsb, ctx.sp)
+                  ptr(row_ptr), ptr(C_col), ptr(C_val), ptr(work), work.numel() * 8, ws, wsb, ctx.sp)
     wstats = None
     if cfg.window_stats and win is not None:
         wrow = win.nwin[:m] > 0

@@ -11,7 +11,7 @@ HEADER = os.path.join(ROOT, "include", "sgb200.h")
 
 def header_functions():
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*|unsigned long long)\s+(sg_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char\*|unsigned long long)\s+(sg_\w+)\(", txt, re.M)))
 
 
 def test_library_exports_every_header_symbol():

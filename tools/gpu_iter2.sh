@@ -1,0 +1,6 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_stress.py -m gpu -q -x > gpurun_out/it_pytest.txt 2>&1; tail -3 gpurun_out/it_pytest.txt
+for lh in 256 0 1024; do
+SG_LIGHT_LEN=$lh timeout 900 python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu > gpurun_out/it_bench_$lh.json 2> gpurun_out/it_bench_$lh.err; python -c "
+import json; d=json.load(open('gpurun_out/it_bench_$lh.json')); print($lh, d['ms_per_step'], d['config']['stage_ms'], d['roofline']['kernel_ms_per_step'])"; tail -2 gpurun_out/it_bench_$lh.err
+done
+timeout 1200 ncu --set full --clock-control none --import-source on -k k_win -c 1 -o gpurun_out/it_prof -f python tools/run_once.py rmat20 > gpurun_out/it_ncu.log 2>&1; tail -1 gpurun_out/it_ncu.log
