@@ -1127,6 +1127,43 @@ __host__ __device__ __forceinline__ int64_t window_capacity(int64_t products, in
   return d / WIN_RP + (span + TILE_COLS) / TILE_COLS / WIN_TILES + 2;
 }
 
+// Count pass of a windowed row (one sweep): word ranks, the saved 16-byte
+// {lo, rank, hi, rank} words and the rank at every tile start in ONE pass
+// over the bitmap (warps own contiguous word ranges; a warp scan of the
+// popcounts gives each word its rank).  tile_rank[t] = rank of tile t's first
+// column relative to the sweep.  Returns the sweep's total.
+template <int NT>
+__device__ __forceinline__ int64_t prefix_save(const unsigned long long* bm, int nwords, int64_t rank_base,
+                                               uint4* __restrict__ dst, int* tile_rank, int64_t* scr) {
+  constexpr int NW = NT / 32;
+  const int w = warp_id(), lane = lane_id();
+  const int per = ((nwords + NW - 1) / NW + 31) & ~31;
+  const int wb = min(nwords, per * w), we = min(nwords, per * (w + 1));
+  int64_t s = 0;
+  for (int i = wb + lane; i < we; i += 32) s += __popcll(bm[i]);
+  s = warp_sum(s);
+  int64_t tot;
+  int64_t base = block_excl_scan(lane == 0 ? s : (int64_t)0, scr, &tot);
+  base = __shfl_sync(SG_FULL, base, 0);
+  for (int i0 = wb; i0 < we; i0 += 32) {
+    const int i = i0 + lane;
+    const unsigned long long wv = i < we ? bm[i] : 0ull;
+    const int c = __popcll(wv);
+    const int inc = warp_incl_scan(c);
+    if (i < we) {
+      const int64_t rel = base + inc - c;
+      if (dst) {
+        const uint32_t r = (uint32_t)(rank_base + rel), lo32 = (uint32_t)wv;
+        st_stream_v4(dst + i, make_uint4(lo32, r, (uint32_t)(wv >> 32), r + (uint32_t)__popc(lo32)));
+      }
+      if ((i & (TILE_WORDS - 1)) == 0) tile_rank[i / TILE_WORDS] = (int)rel;
+    }
+    base += __shfl_sync(SG_FULL, inc, 31);
+  }
+  __syncthreads();
+  return tot;
+}
+
 template <int BW, int MODE, typename V, int NT>
 __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __restrict__ rows, Csr A, Csr B,
                                                const int8_t* kind, const int64_t* cap, const int64_t* alloc,
@@ -1205,7 +1242,15 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
         total += wtot;
         continue;
       }
-      const int64_t wtot = bitmap_prefix<NT>(bm, pre, nwords, scr);
+      // MODE 0 (windowed rows): ranks, saved words and tile ranks in one
+      // pass (pre[t] = rank of tile t); MODE 1: word ranks for the values
+      const int64_t wtot =
+          MODE == 0 ? prefix_save<NT>(bm, nwords, total,
+                                      win.bm_save ? reinterpret_cast<uint4*>(win.bm_save) + win.bm_off[row] +
+                                                        ((wlo - org) >> 6)
+                                                  : nullptr,
+                                      pre, scr)
+                    : bitmap_prefix<NT>(bm, pre, nwords, scr);
       if (MODE == 0) {
         // emit numeric windows.  Tile t (TILE_WORDS words, relative to the
         // tile-aligned origin) belongs to window id = rank(t)/WIN_RP +
@@ -1213,18 +1258,10 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
         // a window starts at every tile whose id differs from the previous.
         const int64_t gw0 = (wlo - org) >> 6;  // count windows are tile-aligned
         int2* wrow = wins + win_off[row];
-        if (win.bm_save) {
-          // keep the row's bitmap with the row rank of every 32-bit half
-          // word, interleaved {lo, rank(lo), hi, rank(hi)} (16 B per 64
-          // columns): the window kernel bulk-copies a window's words into
-          // shared memory as they are (no second key pass, no prefix)
-          uint4* dst = reinterpret_cast<uint4*>(win.bm_save) + win.bm_off[row] + gw0;
-          for (int i = threadIdx.x; i < nwords; i += NT) {
-            const unsigned long long wv = bm[i];
-            const uint32_t r = (uint32_t)(total + pre[i]), lo32 = (uint32_t)wv;
-            st_stream_v4(dst + i, make_uint4(lo32, r, (uint32_t)(wv >> 32), r + (uint32_t)__popc(lo32)));
-          }
-        }
+        // (the row's bitmap was saved by prefix_save with the row rank of
+        // every 32-bit half word, interleaved {lo, rank(lo), hi, rank(hi)}
+        // (16 B per 64 columns): the window kernel bulk-copies a window's
+        // words into shared memory as they are)
         // windows: greedy cuts over the row's tiles in column order -- a
         // window takes tiles while it holds <= WIN_R distinct columns over
         // <= WIN_TILES tiles; warp 0 walks 32 tiles per ballot, one ballot
@@ -1238,8 +1275,8 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
           for (int ti0 = 0; ti0 < ntiles; ti0 += 32) {
             const int ti = ti0 + lane;
             const bool in = ti < ntiles;
-            const int64_t r = in ? total + pre[ti * TILE_WORDS] : 0;
-            const int64_t rn = (ti + 1 < ntiles) ? total + pre[(ti + 1) * TILE_WORDS] : total + wtot;
+            const int64_t r = in ? total + pre[ti] : 0;
+            const int64_t rn = (ti + 1 < ntiles) ? total + pre[ti + 1] : total + wtot;
             const int64_t tg = tg0 + ti;
             int from = 0;
             for (;;) {
@@ -1646,8 +1683,9 @@ constexpr int KW_NT = 1024;
 constexpr int KW_PW = 8;                     // producer warps
 constexpr int KW_CW = KW_NT / 32 - KW_PW;    // consumer warps
 constexpr int KW_NP = KW_PW * 32;            // producer threads (one A entry each per batch)
-constexpr int KW_SEG = 512;                  // segments per chunk
-constexpr int KW_GRP = 512;                  // 32-product groups per chunk
+constexpr int KW_SEG = 256;                  // segments per chunk
+constexpr int KW_GRP = 256;                  // 32-product groups per chunk
+constexpr int KW_NCH = 4;                    // chunk slots (the producer runs up to 4 chunks ahead)
 constexpr int KW_PMAX = 32 * KW_GRP;         // products per chunk
 constexpr int KW_U = 4;                      // groups per consumer step
 static_assert(WIN_R * 8 * 2 + WIN_WORDS * 16 * 2 <= 196608, "two windows in shared memory");
@@ -1660,16 +1698,18 @@ struct KwChunk {
   int32_t S[KW_SEG + 2];   // chunk-relative first product of segment c
   int2 grp[KW_GRP];        // group g: {segment of product 32g, segment starts in (32g, 32g+32)}
   int64_t out_base;        // C index of the window's first entry
-  int32_t P, ng, wslot, flags, c0, cnt, rank0;
+  int32_t P, ng, wslot, flags, c0, cnt, rank0, nwords;
   uint32_t next;           // consumer step counter
 };
 
 struct KwShared {
   double vals[2][WIN_R];
   uint4 bm[2][WIN_WORDS];
-  KwChunk ch[2];
-  unsigned long long full[2], empty[2], bm_full[2], win_free[2];
+  KwChunk ch[KW_NCH];
+  unsigned long long full[KW_NCH], empty[KW_NCH], bm_full[2], win_free[2];
   int win_done[2];
+  unsigned col_next[2];    // column-emission work counter of each window slot
+  WinItem items[4];        // producer's work-item ring (loaded two windows ahead)
   int pscan[KW_PW + 1];
   int pexcl[KW_NP + 1];
   int64_t ticket;
@@ -1700,7 +1740,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         : "r"(a), "r"(parity)
         : "memory");
     if (done) break;
-    __nanosleep(64);
+    __nanosleep(200);
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
@@ -1795,6 +1835,8 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
                                             const Csr& A, const Csr& B, const BTile& bt,
                                             const uint4* __restrict__ bm16, const KwEnt* __restrict__ hent,
                                             unsigned long long* ticket) {
+  (void)A;
+  (void)ticket;
   const int tid = threadIdx.x;  // 0 .. KW_NP-1
   const int lane = lane_id(), pw = warp_id();
   unsigned wseq = 0, cseq = 0;
@@ -1802,12 +1844,24 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   KwChunk* ch = nullptr;
 
   auto acquire = [&]() {
-    const unsigned cs = cseq & 1u;
-    mbar_wait(&sh.empty[cs], ((cseq >> 1) & 1u) ^ 1u);
+    const unsigned cs = cseq % KW_NCH;
+    mbar_wait(&sh.empty[cs], ((cseq / KW_NCH) & 1u) ^ 1u);
     ch = &sh.ch[cs];
     nprod = nseg = 0;
   };
+  bool copy_pending = false;
+  const WinItem* copy_item = nullptr;
+  unsigned copy_slot = 0, copy_wseq = 0;
   auto publish = [&](int flags, const WinItem& it, unsigned wslot) {
+    if (copy_pending) {
+      mbar_wait(&sh.win_free[copy_slot], ((copy_wseq >> 1) & 1u) ^ 1u);
+      if (tid == 0) {
+        const unsigned nwords = (unsigned)(((int64_t)copy_item->c1 - copy_item->c0 + 63) >> 6);
+        mbar_arrive_tx(&sh.bm_full[copy_slot], nwords * 16u);
+        bulk_g2s(&sh.bm[copy_slot][0], bm16 + copy_item->bm_word, nwords * 16u, &sh.bm_full[copy_slot]);
+      }
+      copy_pending = false;
+    }
     // group table of the chunk: owner of every group's first product and
     // the segment starts inside the group (S strictly increasing)
     const int ng = (nprod + 31) >> 5;
@@ -1836,90 +1890,134 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
       ch->c0 = it.c0;
       ch->cnt = it.cnt;
       ch->rank0 = it.rank0;
+      ch->nwords = (int)(((int64_t)it.c1 - it.c0 + 63) >> 6);
       ch->out_base = it.out_base;
       ch->next = 0;
     }
     pbar();
-    if (tid == 0) mbar_arrive(&sh.full[cseq & 1u]);
+    if (tid == 0) mbar_arrive(&sh.full[cseq % KW_NCH]);
     ++cseq;
   };
-
-  for (;;) {
-    if (tid == 0) sh.ticket = (int64_t)atomicAdd(ticket, 1ull);
+  // one batch of KW_NP entries into the chunk(s): scan, append, publish full
+  // chunks.  (bs, len, a) is this thread's clipped segment.
+  auto append = [&](int64_t bs, int len, double a, int& flags, const WinItem& it, unsigned wslot) {
+    const int pk = (len << 9) | (len > 0 ? 1 : 0);  // (length, non-empty)
+    const int inc = warp_incl_scan(pk);
+    if (lane == 31) sh.pscan[pw] = inc;
     pbar();
-    const int64_t b = sh.ticket;
+    int wbase = 0;
+    for (int w = 0; w < pw; ++w) wbase += sh.pscan[w];
+    const int excl = wbase + inc - pk;
+    sh.pexcl[tid] = excl;
+    if (tid == KW_NP - 1) sh.pexcl[KW_NP] = excl + pk;
     pbar();
-    if (b >= nwork) break;
-    const WinItem it = work[b];
-    const unsigned wslot = wseq & 1u;
-    // the window buffers are free once the window two back was stored
-    mbar_wait(&sh.win_free[wslot], ((wseq >> 1) & 1u) ^ 1u);
-    if (tid == 0) {
-      const unsigned nwords = (unsigned)(((int64_t)it.c1 - it.c0 + 63) >> 6);
-      mbar_arrive_tx(&sh.bm_full[wslot], nwords * 16u);
-      bulk_g2s(&sh.bm[wslot][0], bm16 + it.bm_word, nwords * 16u, &sh.bm_full[wslot]);
+    int from = 0;
+    while (from < KW_NP) {
+      const int base = sh.pexcl[from];
+      const int rel_in = excl + pk - base;  // inclusive, relative to `from`
+      const bool fits = tid >= from && nprod + (rel_in >> 9) <= KW_PMAX && nseg + (rel_in & 511) <= KW_SEG;
+      const int nfit = pbar_popc(fits);
+      if (fits && len > 0) {
+        const int rel_ex = excl - base;
+        const int c = nseg + (rel_ex & 511);
+        const int S = nprod + (rel_ex >> 9);
+        ch->S[c] = S;
+        ch->d[c] = bs - S;
+        ch->av[c] = a;
+      }
+      const int tot = sh.pexcl[from + nfit] - base;
+      nprod += tot >> 9;
+      nseg += tot & 511;
+      from += nfit;
+      if (from < KW_NP) {  // chunk full: publish it, continue in the next slot
+        publish(flags, it, wslot);
+        flags = 0;
+        acquire();
+      }
     }
+    pbar();  // pexcl / pscan reuse
+  };
+  auto clip_of = [&](const WinItem& it, int64_t t, int64_t t1, int64_t& bs, int& len, double& a) {
+    bs = 0;
+    len = 0;
+    a = 0.0;
+    if (t < t1) {
+      const KwEnt en = hent[t];
+      kw_clip(en, B.col, bt, it.c0, it.c1, it.last != 0, bs, len);
+      a = en.av;
+    }
+  };
+
+  // Static round-robin over the work items (neighbouring items are alike:
+  // same column bucket).  Software pipeline across windows, three levels
+  // deep: the item two windows ahead is copied into a shared ring, the next
+  // window's entry records are loaded at the top of this window and its
+  // first batch clipped (B tile index) before this window's last publish,
+  // so the dependent global round trips overlap this window's work.
+  const int64_t G = gridDim.x;
+  const int64_t b0 = blockIdx.x;
+  auto load_item = [&](int64_t bb, int slot) {  // 12 threads copy one 48-byte item
+    if (tid < 12 && bb < nwork)
+      reinterpret_cast<int32_t*>(&sh.items[slot])[tid] = reinterpret_cast<const int32_t*>(work + bb)[tid];
+  };
+  load_item(b0, 0);
+  load_item(b0 + G, 1);
+  pbar();
+  int64_t nbs = 0;
+  int nlen = 0;
+  double na = 0.0;
+  if (b0 < nwork) {
+    const WinItem& f = sh.items[0];
+    clip_of(f, f.t0 + tid, f.t0 + f.t_len, nbs, nlen, na);
+  }
+  unsigned k = 0;
+  for (int64_t b = b0; b < nwork; b += G, ++k) {
+    const WinItem it = sh.items[k & 3u];
+    const bool more = b + G < nwork;
+    load_item(b + 2 * G, (k + 2) & 3u);  // visible after this window's barriers
+    KwEnt en_n{0, -1, 0.0, 0, 0};
+    const WinItem& itn = sh.items[(k + 1) & 3u];
+    if (more && tid < itn.t_len) en_n = hent[itn.t0 + tid];
+    const int64_t bs0 = nbs;
+    const int len0 = nlen;
+    const double a0 = na;
+    const unsigned wslot = wseq & 1u;
+    // the window's bitmap is copied into its slot once the window two back
+    // was stored (win_free) -- just before the window's first chunk is
+    // published, so building that chunk overlaps the wait
+    copy_pending = true;
+    copy_item = &sh.items[k & 3u];
+    copy_slot = wslot;
+    copy_wseq = wseq;
     acquire();
     int flags = KW_FIRST;
     const int64_t t0 = it.t0, t1 = it.t0 + it.t_len;
-    for (int64_t tb = t0; tb < t1; tb += KW_NP) {
-      const int64_t t = tb + tid;
-      int64_t bs = 0;
-      int len = 0;
-      double a = 0.0;
-      if (t < t1) {
-        const KwEnt en = hent[t];
-        kw_clip(en, B.col, bt, it.c0, it.c1, it.last != 0, bs, len);
-        a = en.av;
-      }
-      // batch scan of (len << 9 | non-empty)
-      const int pk = (len << 9) | (len > 0 ? 1 : 0);
-      const int inc = warp_incl_scan(pk);
-      if (lane == 31) sh.pscan[pw] = inc;
-      pbar();
-      int wbase = 0;
-      for (int w = 0; w < pw; ++w) wbase += sh.pscan[w];
-      const int excl = wbase + inc - pk;
-      sh.pexcl[tid] = excl;
-      if (tid == KW_NP - 1) sh.pexcl[KW_NP] = excl + pk;
-      pbar();
-      int from = 0;
-      while (from < KW_NP) {
-        const int base = sh.pexcl[from];
-        const int rel_in = excl + pk - base;  // inclusive, relative to `from`
-        const bool fits = tid >= from && nprod + (rel_in >> 9) <= KW_PMAX && nseg + (rel_in & 511) <= KW_SEG;
-        const int nfit = pbar_popc(fits);
-        if (fits && len > 0) {
-          const int rel_ex = excl - base;
-          const int c = nseg + (rel_ex & 511);
-          const int S = nprod + (rel_ex >> 9);
-          ch->S[c] = S;
-          ch->d[c] = bs - S;
-          ch->av[c] = a;
-        }
-        const int tot = sh.pexcl[from + nfit] - base;
-        nprod += tot >> 9;
-        nseg += tot & 511;
-        from += nfit;
-        if (from < KW_NP) {  // chunk full: publish it, continue in the next slot
-          publish(flags, it, wslot);
-          flags = 0;
-          acquire();
-        }
-      }
-      pbar();  // pexcl / pscan reuse
+    append(bs0, len0, a0, flags, it, wslot);
+    for (int64_t tb = t0 + KW_NP; tb < t1; tb += KW_NP) {
+      int64_t bs;
+      int len;
+      double a;
+      clip_of(it, tb + tid, t1, bs, len, a);
+      append(bs, len, a, flags, it, wslot);
+    }
+    nbs = 0;
+    nlen = 0;
+    na = 0.0;
+    if (more && tid < itn.t_len) {  // next window's first batch, in flight over the publish
+      kw_clip(en_n, B.col, bt, itn.c0, itn.c1, itn.last != 0, nbs, nlen);
+      na = en_n.av;
     }
     publish(flags | KW_LAST, it, wslot);
     ++wseq;
   }
   acquire();
-  nprod = nseg = 0;
   WinItem none{};
   publish(KW_END, none, 0);
 }
 
 template <typename V>
-__device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, V* __restrict__ out_val) {
+__device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t* __restrict__ out_col,
+                                            V* __restrict__ out_val) {
   const int lane = lane_id();
   const unsigned le = lanemask_le();
   const int32_t* __restrict__ b_col = B.col;
@@ -1927,12 +2025,13 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, V* __res
   unsigned cseq = 0;
   unsigned wuse[2] = {0u, 0u};
   for (;;) {
-    const unsigned cs = cseq & 1u;
-    mbar_wait(&sh.full[cs], (cseq >> 1) & 1u);
+    const unsigned cs = cseq % KW_NCH;
+    mbar_wait(&sh.full[cs], (cseq / KW_NCH) & 1u);
     KwChunk& ch = sh.ch[cs];
     const int flags = ch.flags;
     if (flags & KW_END) break;
-    const int ng = ch.ng, P = ch.P, ws = ch.wslot, c0 = ch.c0, cnt = ch.cnt, rank0 = ch.rank0;
+    const int ng = ch.ng, P = ch.P, ws = ch.wslot, c0 = ch.c0, cnt = ch.cnt, rank0 = ch.rank0,
+              nwords = ch.nwords;
     const int64_t out_base = ch.out_base;
     if (flags & KW_FIRST) {
       mbar_wait(&sh.bm_full[ws], wuse[ws] & 1u);
@@ -1983,6 +2082,32 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, V* __res
     if (flags & KW_LAST) __threadfence_block();
     if (lane == 0) mbar_arrive(&sh.empty[cs]);
     if (flags & KW_LAST) {
+      // C's columns of the window, straight from the bitmap in shared memory
+      // (its 32-bit halves carry their row rank): every consumer warp that is
+      // done with the window takes 128-half-word slices until none are left
+      if (out_col) {
+        const uint32_t bmw = smem_u32(&sh.bm[ws][0]);
+        const int nh = 2 * nwords;
+        int32_t* oc = out_col + out_base - rank0;
+        for (;;) {
+          unsigned j = 0;
+          if (lane == 0) j = atomicAdd(&sh.col_next[ws], 128u);
+          j = __shfl_sync(SG_FULL, j, 0);
+          if ((int)j >= nh) break;
+          const int hend = min((int)j + 128, nh);
+          for (int h = (int)j + lane; h < hend; h += 32) {
+            const uint2 p = lds_u2(bmw + (uint32_t)h * 8u);
+            unsigned bits = p.x;
+            int32_t* o = oc + p.y;
+            const int32_t cb = c0 + 32 * h;
+            while (bits) {
+              st_stream(o++, cb + __ffs(bits) - 1);
+              bits &= bits - 1;
+            }
+          }
+        }
+      }
+      __threadfence_block();
       int n = 0;
       if (lane == 0) n = atomicAdd(&sh.win_done[ws], 1);
       n = __shfl_sync(SG_FULL, n, 0);
@@ -2011,6 +2136,7 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, V* __res
         __syncwarp();
         if (lane == 0) {
           sh.win_done[ws] = 0;
+          sh.col_next[ws] = 0;
           mbar_arrive(&sh.win_free[ws]);
         }
       }
@@ -2078,18 +2204,21 @@ __global__ void __launch_bounds__(NT) k_win_light(int64_t m, const int32_t* __re
 template <typename V>
 __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* __restrict__ work, Csr A, Csr B,
                                                   BTile bt, const uint4* __restrict__ bm16,
-                                                  const KwEnt* __restrict__ hent, V* __restrict__ out_val,
-                                                  unsigned long long* __restrict__ ticket) {
+                                                  const KwEnt* __restrict__ hent, int32_t* __restrict__ out_col,
+                                                  V* __restrict__ out_val, unsigned long long* __restrict__ ticket) {
   extern __shared__ __align__(128) unsigned char kw_smem[];
   KwShared& sh = *reinterpret_cast<KwShared*>(kw_smem);
   for (int i = threadIdx.x; i < 2 * WIN_R; i += KW_NT) (&sh.vals[0][0])[i] = 0.0;
   if (threadIdx.x == 0) {
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < KW_NCH; ++j) {
       mbar_init(&sh.full[j], 1);
       mbar_init(&sh.empty[j], KW_CW);
+    }
+    for (int j = 0; j < 2; ++j) {
       mbar_init(&sh.bm_full[j], 1);
       mbar_init(&sh.win_free[j], 1);
       sh.win_done[j] = 0;
+      sh.col_next[j] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -2097,7 +2226,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* 
   if (warp_id() < KW_PW)
     kw_producer<V>(sh, nwork, work, A, B, bt, bm16, hent, ticket);
   else
-    kw_consumer<V>(sh, B, out_val);
+    kw_consumer<V>(sh, B, out_col, out_val);
 }
 
 // Column expansion of the long rows from the saved key bitmaps:
@@ -2753,6 +2882,16 @@ static int light_len() {
 }
 
 
+// C's columns of the windowed rows written by k_win itself (1, default) or by
+// the separate expansion kernel (SG_FUSE_COLS=0)
+static bool fuse_cols() {
+  static bool v = [] {
+    const char* e = getenv("SG_FUSE_COLS");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 // window scratch: WinItems, then the heavy and light entry tables (indexed by
 // A position) and their per-row counts
 struct WinScratch {
@@ -2783,13 +2922,14 @@ static WinScratch win_scratch(void* buf, int64_t m, int64_t nnz_a, int64_t nwin)
 
 template <typename V>
 static int launch_kwin(int64_t n, const WinItem* work, const Csr& A, const Csr& B, const BTile& bt, const Win& W,
-                       const KwEnt* hent, void* out_val, unsigned long long* ticket, cudaStream_t s) {
+                       const KwEnt* hent, int32_t* out_col, void* out_val, unsigned long long* ticket,
+                       cudaStream_t s) {
   constexpr size_t sm = sizeof(KwShared);
   auto kern = k_win<V>;
   if (int rc = set_smem(kern, sm)) return rc;
   const int grid = (int)std::min<int64_t>(n, (int64_t)num_sms());
-  kern<<<grid, KW_NT, sm, s>>>(n, work, A, B, bt, reinterpret_cast<const uint4*>(W.bm_save), hent, (V*)out_val,
-                               ticket);
+  kern<<<grid, KW_NT, sm, s>>>(n, work, A, B, bt, reinterpret_cast<const uint4*>(W.bm_save), hent, out_col,
+                               (V*)out_val, ticket);
   return check_cuda("k_win");
 }
 
@@ -2992,7 +3132,7 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
                                                  out_off, W.bm_save ? W.bm_off : nullptr,
                                                  W.bm_save ? wsc.hcnt : nullptr, cnt, work);
   if (int rc = check_cuda("k_win_scatter")) return rc;
-  if (W.bm_save) {
+  if (W.bm_save && !fuse_cols()) {
     ktimer_begin("k_expand", s);
     k_expand_rank<EXP_NT, 4, 6144><<<(int)std::min<int64_t>(nwork, (int64_t)num_sms() * 4), EXP_NT, 0, s>>>(
         nwork, work, reinterpret_cast<const uint4*>(W.bm_save), out_col);
@@ -3006,8 +3146,9 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   if (W.bm_save) {
     // saved bitmaps: the warp-specialised window kernel takes every window
     // (both size classes, in ticket order), heavy entries only
-    int rc = dtype == SG_F64 ? launch_kwin<double>(nwork, work, A, B, bt, W, wsc.hent, out_val, tickets, s)
-                             : launch_kwin<float>(nwork, work, A, B, bt, W, wsc.hent, out_val, tickets, s);
+    int32_t* kcol = fuse_cols() ? out_col : nullptr;
+    int rc = dtype == SG_F64 ? launch_kwin<double>(nwork, work, A, B, bt, W, wsc.hent, kcol, out_val, tickets, s)
+                             : launch_kwin<float>(nwork, work, A, B, bt, W, wsc.hent, kcol, out_val, tickets, s);
     if (rc) return rc;
     ktimer_end(s);
     // then the light entries add on top of the stored window values
@@ -3060,10 +3201,10 @@ int sg_btile_plan(int64_t k, int64_t b_ncols, const int64_t* b_ptr, int64_t budg
   unsigned long long hh[64];
   cudaMemcpyAsync(hh, hist, sizeof(hh), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_btile_plan sync", 0);
-  // smallest power-of-two length class (>= 32) whose rows fit the budget
+  // smallest power-of-two length class whose rows (and all longer ones) fit the budget
   int cls = 63;
   int64_t rows = 0;
-  for (int c = 63; c >= 5; --c) {
+  for (int c = 63; c >= 0; --c) {  // down to single-entry rows while the budget lasts
     if ((rows + (int64_t)hh[c]) * per_row * 4 > budget_bytes) break;
     rows += (int64_t)hh[c];
     cls = c;

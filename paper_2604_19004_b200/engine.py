@@ -320,7 +320,7 @@ def release_bitmap_arena(device=None):
 
 
 # the B tile index (sg_btile_plan) may use at most this many bytes
-BTILE_BUDGET = 1 << 30
+BTILE_BUDGET = 2 << 30
 
 
 def btile(ctx: _Ctx, B: DeviceCsr, win: Windows):
