@@ -34,6 +34,8 @@
 
 #include <cub/block/block_radix_sort.cuh>
 #include <string>
+#include <vector>
+#include <cstdio>
 
 #include "sg_internal.cuh"
 
@@ -1456,6 +1458,7 @@ __device__ __forceinline__ void emit_bits32_smem(uint32_t bits, int32_t colbase,
 #ifdef SG_PROF
 // phase cycle counters of the window kernel (profiling build only: make prof)
 __device__ unsigned long long g_phase[12];
+__device__ unsigned long long g_kw[16];  // k_win: producer / consumer phase cycles
 #define SG_PH(i)                                              \
   if (threadIdx.x == 0) {                                     \
     const long long _t = clock64();                           \
@@ -1679,13 +1682,29 @@ __global__ void __launch_bounds__(NT, CTAS) k_bmr(int64_t nwork, const WinItem* 
 // Reference: the long-row part of _numeric_phase / _fallback_phase
 // (engine.py:252-328), fallback_accumulate (accumulate.py:274-279).
 
+#ifdef SG_PROF
+#define KW_T0() const long long _kt0 = clock64()
+#define KW_ACC(acc) (acc) += (unsigned long long)(clock64() - _kt0)
+#else
+#define KW_T0()
+#define KW_ACC(acc)
+#endif
 constexpr int KW_NT = 1024;
-constexpr int KW_PW = 8;                     // producer warps
+#ifndef SG_KW_PW
+#define SG_KW_PW 8
+#endif
+#ifndef SG_KW_SEG
+#define SG_KW_SEG 256
+#endif
+#ifndef SG_KW_NCH
+#define SG_KW_NCH 4
+#endif
+constexpr int KW_PW = SG_KW_PW;              // producer warps
 constexpr int KW_CW = KW_NT / 32 - KW_PW;    // consumer warps
 constexpr int KW_NP = KW_PW * 32;            // producer threads (one A entry each per batch)
-constexpr int KW_SEG = 256;                  // segments per chunk
-constexpr int KW_GRP = 256;                  // 32-product groups per chunk
-constexpr int KW_NCH = 4;                    // chunk slots (the producer runs up to 4 chunks ahead)
+constexpr int KW_SEG = SG_KW_SEG;            // segments per chunk
+constexpr int KW_GRP = SG_KW_SEG;            // 32-product groups per chunk
+constexpr int KW_NCH = SG_KW_NCH;            // chunk slots (the producer runs up to KW_NCH chunks ahead)
 constexpr int KW_PMAX = 32 * KW_GRP;         // products per chunk
 constexpr int KW_U = 4;                      // groups per consumer step
 static_assert(WIN_R * 8 * 2 + WIN_WORDS * 16 * 2 <= 196608, "two windows in shared memory");
@@ -1797,7 +1816,7 @@ __global__ void __launch_bounds__(NT) k_win_entries(int64_t m, const int32_t* __
         e.len = (int32_t)(b_ptr[k + 1] - e.bs);
         e.to = bt.off ? bt.off[k] : -1;
         e.av = (double)av[t + threadIdx.x];
-        kind = e.len >= lh ? 1 : (e.len > 0 ? 2 : 0);
+        kind = e.len <= 0 ? 0 : (e.len >= lh ? 1 : 2);  // empty B rows contribute nothing
       }
       int64_t tot;
       const int64_t ex = block_excl_scan((int64_t)(kind == 1) | ((int64_t)(kind == 2) << 32), scr, &tot);
@@ -1843,9 +1862,13 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   int nprod = 0, nseg = 0;
   KwChunk* ch = nullptr;
 
+  unsigned long long pc_free = 0, pc_empty = 0, pc_append = 0, pc_pub = 0, pc_clip = 0;
+  (void)pc_free; (void)pc_empty; (void)pc_append; (void)pc_pub; (void)pc_clip;
   auto acquire = [&]() {
     const unsigned cs = cseq % KW_NCH;
+    KW_T0();
     mbar_wait(&sh.empty[cs], ((cseq / KW_NCH) & 1u) ^ 1u);
+    KW_ACC(pc_empty);
     ch = &sh.ch[cs];
     nprod = nseg = 0;
   };
@@ -1854,7 +1877,9 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   unsigned copy_slot = 0, copy_wseq = 0;
   auto publish = [&](int flags, const WinItem& it, unsigned wslot) {
     if (copy_pending) {
+      KW_T0();
       mbar_wait(&sh.win_free[copy_slot], ((copy_wseq >> 1) & 1u) ^ 1u);
+      KW_ACC(pc_free);
       if (tid == 0) {
         const unsigned nwords = (unsigned)(((int64_t)copy_item->c1 - copy_item->c0 + 63) >> 6);
         mbar_arrive_tx(&sh.bm_full[copy_slot], nwords * 16u);
@@ -1864,6 +1889,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
     }
     // group table of the chunk: owner of every group's first product and
     // the segment starts inside the group (S strictly increasing)
+    KW_T0();
     const int ng = (nprod + 31) >> 5;
     if (tid == 0) ch->S[nseg] = nprod;
     pbar();
@@ -1897,10 +1923,12 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
     pbar();
     if (tid == 0) mbar_arrive(&sh.full[cseq % KW_NCH]);
     ++cseq;
+    KW_ACC(pc_pub);
   };
   // one batch of KW_NP entries into the chunk(s): scan, append, publish full
   // chunks.  (bs, len, a) is this thread's clipped segment.
   auto append = [&](int64_t bs, int len, double a, int& flags, const WinItem& it, unsigned wslot) {
+    KW_T0();
     const int pk = (len << 9) | (len > 0 ? 1 : 0);  // (length, non-empty)
     const int inc = warp_incl_scan(pk);
     if (lane == 31) sh.pscan[pw] = inc;
@@ -1936,6 +1964,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
       }
     }
     pbar();  // pexcl / pscan reuse
+    KW_ACC(pc_append);
   };
   auto clip_of = [&](const WinItem& it, int64_t t, int64_t t1, int64_t& bs, int& len, double& a) {
     bs = 0;
@@ -1949,84 +1978,136 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   };
 
   // Static round-robin over the work items (neighbouring items are alike:
-  // same column bucket).  Software pipeline across windows, three levels
-  // deep: the item two windows ahead is copied into a shared ring, the next
-  // window's entry records are loaded at the top of this window and its
-  // first batch clipped (B tile index) before this window's last publish,
-  // so the dependent global round trips overlap this window's work.
+  // same column bucket).  The producer walks the flattened sequence of
+  // entry batches (KW_NP entries of one window; every window has >= 1) as a
+  // three-stage software pipeline: at each step the entry records of the
+  // batch two ahead are loaded, the batch one ahead is clipped (B tile index
+  // loads in flight), and the current batch -- clipped one step ago -- is
+  // scanned and appended.  The dependent global round trips (entry record,
+  // then tile index) thus overlap two steps of barrier / shared-memory work.
+  // Work items live in a 4-entry shared ring, loaded three windows ahead.
   const int64_t G = gridDim.x;
   const int64_t b0 = blockIdx.x;
-  auto load_item = [&](int64_t bb, int slot) {  // 12 threads copy one 48-byte item
-    if (tid < 12 && bb < nwork)
-      reinterpret_cast<int32_t*>(&sh.items[slot])[tid] = reinterpret_cast<const int32_t*>(work + bb)[tid];
+  const int64_t nmine = b0 < nwork ? (nwork - 1 - b0) / G + 1 : 0;  // windows of this CTA
+  auto load_item = [&](int64_t k) {  // 12 threads copy one 48-byte item into the ring
+    const int64_t bb = b0 + k * G;
+    if (tid < 12 && k < nmine)
+      reinterpret_cast<int32_t*>(&sh.items[k & 3])[tid] = reinterpret_cast<const int32_t*>(work + bb)[tid];
   };
-  load_item(b0, 0);
-  load_item(b0 + G, 1);
+  for (int64_t k = 0; k < 3; ++k) load_item(k);
   pbar();
-  int64_t nbs = 0;
-  int nlen = 0;
-  double na = 0.0;
-  if (b0 < nwork) {
-    const WinItem& f = sh.items[0];
-    clip_of(f, f.t0 + tid, f.t0 + f.t_len, nbs, nlen, na);
+  // batch cursor: window k (of this CTA), first entry offset tb within it
+  struct Cur {
+    int64_t k;
+    int tb;
+  };
+  auto advance = [&](Cur c) {
+    const WinItem& w = sh.items[c.k & 3];
+    if (c.tb + KW_NP < w.t_len) return Cur{c.k, c.tb + KW_NP};
+    return Cur{c.k + 1, 0};
+  };
+  auto load_ent = [&](Cur c, KwEnt& e) {
+    e = KwEnt{0, -1, 0.0, 0, 0};
+    if (c.k < nmine) {
+      const WinItem& w = sh.items[c.k & 3];
+      if (c.tb + tid < w.t_len) e = hent[w.t0 + c.tb + tid];
+    }
+  };
+  auto clip_ent = [&](Cur c, const KwEnt& e, int64_t& bs, int& len, double& a) {
+    bs = 0;
+    len = 0;
+    a = 0.0;
+    if (c.k < nmine && e.len > 0) {
+      const WinItem& w = sh.items[c.k & 3];
+      kw_clip(e, B.col, bt, w.c0, w.c1, w.last != 0, bs, len);
+      a = e.av;
+    }
+  };
+  Cur c0{0, 0}, c1 = c0, c2 = c0;
+  KwEnt e1, e2;
+  int64_t bs0 = 0;
+  int len0 = 0;
+  double a0 = 0.0;
+  if (nmine > 0) {
+    c1 = advance(c0);
+    c2 = c1.k < nmine ? advance(c1) : c1;
+    KwEnt e0;
+    load_ent(c0, e0);
+    load_ent(c1, e1);
+    clip_ent(c0, e0, bs0, len0, a0);
   }
-  unsigned k = 0;
-  for (int64_t b = b0; b < nwork; b += G, ++k) {
-    const WinItem it = sh.items[k & 3u];
-    const bool more = b + G < nwork;
-    load_item(b + 2 * G, (k + 2) & 3u);  // visible after this window's barriers
-    KwEnt en_n{0, -1, 0.0, 0, 0};
-    const WinItem& itn = sh.items[(k + 1) & 3u];
-    if (more && tid < itn.t_len) en_n = hent[itn.t0 + tid];
-    const int64_t bs0 = nbs;
-    const int len0 = nlen;
-    const double a0 = na;
+  int flags = 0;
+  int64_t kcur = -1;
+  while (c0.k < nmine) {
+    // new window: fresh chunk, bitmap copy pending until its first publish,
+    // ring slot of the window three ahead refilled
+    if (c0.k != kcur) {
+      kcur = c0.k;
+      load_item(kcur + 3);
+      copy_pending = true;
+      copy_item = &sh.items[kcur & 3];
+      copy_slot = wseq & 1u;
+      copy_wseq = wseq;
+      acquire();
+      flags = KW_FIRST;
+    }
+    load_ent(c2, e2);                  // stage 0: records of the batch two ahead
+    int64_t bs1;
+    int len1;
+    double a1;
+    {
+      KW_T0();
+      clip_ent(c1, e1, bs1, len1, a1);  // stage 1: tile-index loads in flight
+      KW_ACC(pc_clip);
+    }
+    const WinItem it = sh.items[c0.k & 3];
     const unsigned wslot = wseq & 1u;
-    // the window's bitmap is copied into its slot once the window two back
-    // was stored (win_free) -- just before the window's first chunk is
-    // published, so building that chunk overlaps the wait
-    copy_pending = true;
-    copy_item = &sh.items[k & 3u];
-    copy_slot = wslot;
-    copy_wseq = wseq;
-    acquire();
-    int flags = KW_FIRST;
-    const int64_t t0 = it.t0, t1 = it.t0 + it.t_len;
-    append(bs0, len0, a0, flags, it, wslot);
-    for (int64_t tb = t0 + KW_NP; tb < t1; tb += KW_NP) {
-      int64_t bs;
-      int len;
-      double a;
-      clip_of(it, tb + tid, t1, bs, len, a);
-      append(bs, len, a, flags, it, wslot);
+    append(bs0, len0, a0, flags, it, wslot);  // stage 2
+    if (c1.k != c0.k) {  // c0 was the window's last batch
+      publish(flags | KW_LAST, it, wslot);
+      ++wseq;
     }
-    nbs = 0;
-    nlen = 0;
-    na = 0.0;
-    if (more && tid < itn.t_len) {  // next window's first batch, in flight over the publish
-      kw_clip(en_n, B.col, bt, itn.c0, itn.c1, itn.last != 0, nbs, nlen);
-      na = en_n.av;
-    }
-    publish(flags | KW_LAST, it, wslot);
-    ++wseq;
+    c0 = c1;
+    bs0 = bs1;
+    len0 = len1;
+    a0 = a1;
+    c1 = c2;
+    e1 = e2;
+    c2 = c2.k < nmine ? advance(c2) : c2;
   }
   acquire();
   WinItem none{};
   publish(KW_END, none, 0);
+#ifdef SG_PROF
+  if (tid == 0) {
+    atomicAdd(&g_kw[0], pc_free);
+    atomicAdd(&g_kw[1], pc_empty);
+    atomicAdd(&g_kw[2], pc_append);
+    atomicAdd(&g_kw[3], pc_pub);
+    atomicAdd(&g_kw[4], pc_clip);
+    atomicAdd(&g_kw[5], (unsigned long long)wseq);
+  }
+#endif
 }
 
 template <typename V>
 __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t* __restrict__ out_col,
-                                            V* __restrict__ out_val) {
+                                            V* __restrict__ out_val, int kw_skip) {
   const int lane = lane_id();
   const unsigned le = lanemask_le();
   const int32_t* __restrict__ b_col = B.col;
   const V* __restrict__ b_val = (const V*)B.val;
   unsigned cseq = 0;
   unsigned wuse[2] = {0u, 0u};
+  unsigned long long cc_full = 0, cc_bm = 0, cc_grp = 0, cc_col = 0, cc_store = 0;
+  (void)cc_full; (void)cc_bm; (void)cc_grp; (void)cc_col; (void)cc_store;
   for (;;) {
     const unsigned cs = cseq % KW_NCH;
-    mbar_wait(&sh.full[cs], (cseq / KW_NCH) & 1u);
+    {
+      KW_T0();
+      mbar_wait(&sh.full[cs], (cseq / KW_NCH) & 1u);
+      KW_ACC(cc_full);
+    }
     KwChunk& ch = sh.ch[cs];
     const int flags = ch.flags;
     if (flags & KW_END) break;
@@ -2034,9 +2115,14 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
               nwords = ch.nwords;
     const int64_t out_base = ch.out_base;
     if (flags & KW_FIRST) {
+      KW_T0();
       mbar_wait(&sh.bm_full[ws], wuse[ws] & 1u);
       ++wuse[ws];
+      KW_ACC(cc_bm);
     }
+#ifdef SG_PROF
+    const long long _kg = clock64();
+#endif
     WinAddOp op{smem_u32(&sh.bm[ws][0]), smem_u32(&sh.vals[ws][0]) - (uint32_t)rank0 * 8u, c0};
     const uint32_t grp_s = smem_u32(&ch.grp[0]), d_s = smem_u32(&ch.d[0]), av_s = smem_u32(&ch.av[0]);
     for (;;) {
@@ -2044,6 +2130,7 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
       if (lane == 0) g0 = atomicAdd(&ch.next, (unsigned)KW_U);
       g0 = __shfl_sync(SG_FULL, g0, 0);
       if ((int)g0 >= ng) break;
+      if (kw_skip) continue;  // timing experiment: producer-bound time (SG_KW_SKIP=1)
       int32_t col[KW_U];
       double v[KW_U];
       if (((int)g0 + KW_U) * 32 <= P) {
@@ -2078,6 +2165,9 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
           if (ok[u]) op(col[u], v[u]);
       }
     }
+#ifdef SG_PROF
+    cc_grp += (unsigned long long)(clock64() - _kg);
+#endif
     __syncwarp();
     if (flags & KW_LAST) __threadfence_block();
     if (lane == 0) mbar_arrive(&sh.empty[cs]);
@@ -2085,6 +2175,7 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
       // C's columns of the window, straight from the bitmap in shared memory
       // (its 32-bit halves carry their row rank): every consumer warp that is
       // done with the window takes 128-half-word slices until none are left
+      KW_T0();
       if (out_col) {
         const uint32_t bmw = smem_u32(&sh.bm[ws][0]);
         const int nh = 2 * nwords;
@@ -2095,23 +2186,43 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
           j = __shfl_sync(SG_FULL, j, 0);
           if ((int)j >= nh) break;
           const int hend = min((int)j + 128, nh);
-          for (int h = (int)j + lane; h < hend; h += 32) {
-            const uint2 p = lds_u2(bmw + (uint32_t)h * 8u);
-            unsigned bits = p.x;
-            int32_t* o = oc + p.y;
-            const int32_t cb = c0 + 32 * h;
-            while (bits) {
-              st_stream(o++, cb + __ffs(bits) - 1);
-              bits &= bits - 1;
+          for (int h0 = (int)j; h0 < hend; h0 += 32) {
+            const int h = h0 + lane;
+            uint2 p = make_uint2(0u, 0u);
+            if (h < hend) p = lds_u2(bmw + (uint32_t)h * 8u);
+            const int mx = (int)__reduce_max_sync(SG_FULL, (unsigned)__popc(p.x));
+            if (mx <= 6) {
+              // sparse half-words: each lane writes its few columns (the
+              // lanes' ranges are adjacent, so the stores are near-coalesced)
+              unsigned bits = p.x;
+              int32_t* o = oc + p.y;
+              const int32_t cb = c0 + 32 * h;
+              while (bits) {
+                st_stream(o++, cb + __ffs(bits) - 1);
+                bits &= bits - 1;
+              }
+            } else {
+              // dense: the warp writes one half-word at a time, lane = bit,
+              // one coalesced store of up to 32 columns each
+              const unsigned below = (1u << lane) - 1u;
+              for (int q = 0; q < 32; ++q) {
+                const unsigned bits = __shfl_sync(SG_FULL, p.x, q);
+                if (!bits) continue;
+                const unsigned r = __shfl_sync(SG_FULL, p.y, q);
+                if (bits >> lane & 1u)
+                  st_stream(oc + r + __popc(bits & below), c0 + 32 * (h0 + q) + lane);
+              }
             }
           }
         }
       }
+      KW_ACC(cc_col);
       __threadfence_block();
       int n = 0;
       if (lane == 0) n = atomicAdd(&sh.win_done[ws], 1);
       n = __shfl_sync(SG_FULL, n, 0);
       if (n == KW_CW - 1) {
+        KW_T0();
         // last warp out: store the window's values (coalesced, streaming)
         // and zero them for the window after next
         const uint32_t vs = smem_u32(&sh.vals[ws][0]);
@@ -2139,10 +2250,21 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
           sh.col_next[ws] = 0;
           mbar_arrive(&sh.win_free[ws]);
         }
+        KW_ACC(cc_store);
       }
     }
     ++cseq;
   }
+#ifdef SG_PROF
+  if (lane == 0) {
+    atomicAdd(&g_kw[8], cc_full);
+    atomicAdd(&g_kw[9], cc_bm);
+    atomicAdd(&g_kw[10], cc_grp);
+    atomicAdd(&g_kw[11], cc_col);
+    atomicAdd(&g_kw[12], cc_store);
+    atomicAdd(&g_kw[13], (unsigned long long)cseq);
+  }
+#endif
 }
 
 // Light entries of the windowed rows: products of B rows shorter than lh
@@ -2205,7 +2327,8 @@ template <typename V>
 __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* __restrict__ work, Csr A, Csr B,
                                                   BTile bt, const uint4* __restrict__ bm16,
                                                   const KwEnt* __restrict__ hent, int32_t* __restrict__ out_col,
-                                                  V* __restrict__ out_val, unsigned long long* __restrict__ ticket) {
+                                                  V* __restrict__ out_val, unsigned long long* __restrict__ ticket,
+                                                  int kw_skip) {
   extern __shared__ __align__(128) unsigned char kw_smem[];
   KwShared& sh = *reinterpret_cast<KwShared*>(kw_smem);
   for (int i = threadIdx.x; i < 2 * WIN_R; i += KW_NT) (&sh.vals[0][0])[i] = 0.0;
@@ -2226,7 +2349,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* 
   if (warp_id() < KW_PW)
     kw_producer<V>(sh, nwork, work, A, B, bt, bm16, hent, ticket);
   else
-    kw_consumer<V>(sh, B, out_col, out_val);
+    kw_consumer<V>(sh, B, out_col, out_val, kw_skip);
 }
 
 // Column expansion of the long rows from the saved key bitmaps:
@@ -2837,6 +2960,12 @@ template <int MODE, typename V>
 static int run_bins(const Launch& L, int64_t m, Workspace& w, const int32_t* rowmap_unused) {
   int64_t cnt[NBINS], off[NBINS + 1];
   if (int rc = partition_rows(m, NBINS, w, cnt, off, L.s)) return rc;
+  if (getenv("SG_PRINT_BINS")) {  // analysis hook: rows per accumulator bin
+    fprintf(stderr, "bins(mode %d):", MODE);
+    for (int b = 0; b < NBINS; ++b)
+      if (cnt[b]) fprintf(stderr, " %d:%lld", b, (long long)cnt[b]);
+    fprintf(stderr, "\n");
+  }
   int nonempty = 0;
   for (int b : kOrder) nonempty += cnt[b] != 0;
   Fork f(L.s);
@@ -2928,8 +3057,12 @@ static int launch_kwin(int64_t n, const WinItem* work, const Csr& A, const Csr& 
   auto kern = k_win<V>;
   if (int rc = set_smem(kern, sm)) return rc;
   const int grid = (int)std::min<int64_t>(n, (int64_t)num_sms());
+  static const int skip = [] {
+    const char* e = getenv("SG_KW_SKIP");
+    return e ? atoi(e) : 0;
+  }();
   kern<<<grid, KW_NT, sm, s>>>(n, work, A, B, bt, reinterpret_cast<const uint4*>(W.bm_save), hent, out_col,
-                               (V*)out_val, ticket);
+                               (V*)out_val, ticket, skip);
   return check_cuda("k_win");
 }
 
@@ -3139,6 +3272,16 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
     ktimer_end(s);
     if (int rc = check_cuda("k_expand")) return rc;
   }
+  if (const char* dump = getenv("SG_DUMP_WINDOWS")) {
+    // analysis hook: the window work items as raw 48-byte records
+    std::vector<WinItem> hw((size_t)nwork);
+    cudaMemcpyAsync(hw.data(), work, (size_t)nwork * sizeof(WinItem), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (FILE* f = fopen(dump, "wb")) {
+      fwrite(hw.data(), sizeof(WinItem), hw.size(), f);
+      fclose(f);
+    }
+  }
   // tickets live after the cursors (the host copy above must finish first)
   unsigned long long* tickets = cnt + 2 * NBUCKET;
   cudaMemsetAsync(tickets, 0, 2 * sizeof(unsigned long long), s);
@@ -3231,6 +3374,13 @@ int sg_btile_build(int64_t k, int64_t b_ncols, const int64_t* b_ptr, const int32
 }
 
 #ifdef SG_PROF
+int sg_debug_kw_cycles(unsigned long long* out16) {
+  cudaMemcpyFromSymbol(out16, g_kw, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_kw, z, sizeof(z));
+  return check_cuda("sg_debug_kw_cycles", 0);
+}
+
 int sg_debug_phase_cycles(unsigned long long* out12) {
   cudaMemcpyFromSymbol(out12, g_phase, sizeof(unsigned long long) * 12);
   unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
