@@ -337,7 +337,7 @@ def check_parity(a, b, rows, cb):
             "row_blocks": [list(x) for x in rows]}
 
 
-TIMED_KERNELS = ("k_bmr", "k_win_light", "k_expand", "k_hash_warp", "k_hash_block", "k_bitmap",
+TIMED_KERNELS = ("k_win", "k_bmr", "k_win_light", "k_expand", "k_hash_warp", "k_hash_block", "k_bitmap",
                  "k_hash_warp:count", "k_hash_block:count", "k_bitmap:count")
 
 
@@ -553,15 +553,18 @@ def main():
     dk = ncu_dominant(args.config)
     if dk not in ktimes:
         dk = max(ktimes, key=lambda kk: ktimes[kk][0]) if ktimes else None
-    if dk == "k_bmr" and n_gpus == 1:
+    if dk in ("k_win", "k_bmr") and n_gpus == 1:
         # the window kernel: algorithmic bytes of the rows it processes (one
         # extra untimed call collects their totals), over its event-timed
         # average launch duration
         c_ws, rs = spgemm(A, B, replace(cfg, window_stats=True))
         del c_ws  # C is >100 GB at R-MAT-20: free it before the e2e run
         ws_ = rs.window_stats
+        # k_win writes both halves of the windows' C entries (columns from
+        # its bitmap, values); k_bmr with saved bitmaps only the values
+        cbytes = (4 + vbytes) if (dk == "k_win" or not ws_["saved_bitmaps"]) else vbytes
         kb = (16 * ws_["rows"] + (4 + vbytes) * ws_["nnz_a"] + (4 + vbytes) * ws_["products"]
-              + (vbytes if ws_["saved_bitmaps"] else 4 + vbytes) * ws_["nnz_c"])
+              + cbytes * ws_["nnz_c"])
         kms_, kn_ = ktimes[dk]
         ach = kb / (kms_ / kn_ * 1e-3) / 1e9
         traffic = ncu_traffic(args.config, dk, kn_ / args.steps)
@@ -570,8 +573,7 @@ def main():
                 "algorithmic_bytes_per_launch": kb, "ms_per_launch": kms_ / kn_,
                 "share_of_step": kms_ / ms_tot,
                 "units_per_launch": {kk: ws_[kk] for kk in ("rows", "windows", "nnz_a", "products", "nnz_c")},
-                "bytes_per_unit": f"16/row + {4 + vbytes}/A entry + {4 + vbytes}/product + "
-                                  f"{vbytes if ws_['saved_bitmaps'] else 4 + vbytes}/C entry",
+                "bytes_per_unit": f"16/row + {4 + vbytes}/A entry + {4 + vbytes}/product + {cbytes}/C entry",
                 "traffic_source": "profiles/ncu_traffic.json (ncu launch list of the same command)",
                 "whole_pass": {"achieved": achieved, "frac": (achieved / peak) if achieved else None,
                                "algorithmic_bytes_per_step": alg}}

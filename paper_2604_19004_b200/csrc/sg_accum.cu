@@ -3285,7 +3285,7 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   // tickets live after the cursors (the host copy above must finish first)
   unsigned long long* tickets = cnt + 2 * NBUCKET;
   cudaMemsetAsync(tickets, 0, 2 * sizeof(unsigned long long), s);
-  ktimer_begin("k_bmr", s);
+  ktimer_begin(W.bm_save ? "k_win" : "k_bmr", s);
   if (W.bm_save) {
     // saved bitmaps: the warp-specialised window kernel takes every window
     // (both size classes, in ticket order), heavy entries only

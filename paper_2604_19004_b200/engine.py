@@ -28,6 +28,7 @@ from dataclasses import dataclass, replace
 
 import numpy as np
 import torch
+from torch.cuda import nvtx as _nvtx
 
 from . import _lib
 from .config import (DEFAULT_SAMPLE_MAX, DEFAULT_SAMPLE_MIN, PRECISION_FOR, EngineConfig,
@@ -467,6 +468,7 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     # ---- analysis (analysis.py:96-128)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     ev[0].record(ctx.stream)
+    _nvtx.range_push("spgemm:analysis")  # reference stage (engine.py:147-216)
     t0 = time.perf_counter()
     products, span_lo, span_hi, totals = row_stats(ctx, A, B)
     tot = totals.cpu().numpy()
@@ -475,6 +477,8 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     er = total_products / nnz_a if nnz_a else 0.0
     avg = total_products / m if m else 0.0
     ev[1].record(ctx.stream)
+    _nvtx.range_pop()
+    _nvtx.range_push("spgemm:sketch")  # reference stage (engine.py:147-216)
     _check_deadline(deadline)
 
     # ---- sketch + sampled CR (engine.py:157-174)
@@ -519,6 +523,8 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         else:
             kind_wf = select_workflow(avg, er, cr[0])
     ev[2].record(ctx.stream)
+    _nvtx.range_pop()
+    _nvtx.range_push("spgemm:predict")  # reference stage (engine.py:147-216)
     _check_deadline(deadline)
 
     # ---- size prediction (predict.py)
@@ -555,6 +561,8 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         pred = products
         pred_kind = "upper_bound"
     ev[3].record(ctx.stream)
+    _nvtx.range_pop()
+    _nvtx.range_push("spgemm:numeric")  # reference stage (engine.py:147-216)
     _check_deadline(deadline)
 
     # ---- binning (accumulate.plan_rows) + numeric phase (engine._numeric_phase)
@@ -640,6 +648,8 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         if short is not None:
             overflow |= ovf
     ev[4].record(ctx.stream)
+    _nvtx.range_pop()
+    _nvtx.range_push("spgemm:fallback")  # reference stage (engine.py:147-216)
     _check_deadline(deadline)
 
     # ---- fallback (engine._fallback_phase): overflow | planned FALLBACK rows
@@ -686,6 +696,8 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         _lib.call("sg_fallback", 1, n_rest, ptr(rest), n, dcode, *fargs, ptr(row_ptr),
                   ptr(C_col), ptr(C_val), ptr(counts), None, ws, wsb, ctx.sp)
     ev[5].record(ctx.stream)
+    _nvtx.range_pop()
+    _nvtx.range_push("spgemm:compact")  # reference stage (engine.py:147-216)
     _check_deadline(deadline)
 
     # ---- post-processing: hash rows were sorted in-kernel; compact the slab
@@ -704,6 +716,7 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         row_ptr = torch.zeros(1, dtype=torch.int64, device=ctx.device)
         nnz_c = 0
     ev[6].record(ctx.stream)
+    _nvtx.range_pop()
     ctx.sync()
     for i, name in enumerate(("analysis", "sketch", "predict", "numeric", "fallback", "compact")):
         kms[name] = ev[i].elapsed_time(ev[i + 1])

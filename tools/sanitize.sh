@@ -6,7 +6,7 @@
 mkdir -p gpurun_out
 for tool in memcheck racecheck synccheck initcheck; do
   extra=""
-  [ "$tool" = "memcheck" ] && extra="--leak-check full"
+  # (no leak check: the torch caching allocator keeps its pool until exit by design)
   [ "$tool" = "racecheck" ] && extra="--racecheck-report hazard"
   timeout 3000 compute-sanitizer --tool $tool $extra --print-limit 200 --error-exitcode 9 \
       python tools/sanitize_cases.py > gpurun_out/sanitize_$tool.txt 2>&1
