@@ -235,7 +235,12 @@ __device__ __forceinline__ void block_products(const Entries& E, int nent, int64
   const uint32_t grp_s = smem_u32(g_grp), d_s = smem_u32(E.d), av_s = smem_u32(E.av);
   const int nw = blockDim.x >> 5, w = warp_id(), lane = lane_id();
   const unsigned le = lanemask_le();
-  constexpr int U = SG_UNR;
+#ifndef SG_UNR_KEYS
+#define SG_UNR_KEYS 8
+#endif
+  // key passes carry a column per product (values passes a column and a
+  // value): twice the gathers in flight at the same register budget
+  constexpr int U = VALUES ? SG_UNR : SG_UNR_KEYS;
   for (int64_t base = 0; base < P; base += 32 * (int64_t)GRP_MAX) {
     const int rem = (int)min((int64_t)32 * GRP_MAX, P - base);  // products of this sub-chunk
     const int ng = (rem + 31) >> 5;
@@ -1706,7 +1711,13 @@ constexpr int KW_SEG = SG_KW_SEG;            // segments per chunk
 constexpr int KW_GRP = SG_KW_SEG;            // 32-product groups per chunk
 constexpr int KW_NCH = SG_KW_NCH;            // chunk slots (the producer runs up to KW_NCH chunks ahead)
 constexpr int KW_PMAX = 32 * KW_GRP;         // products per chunk
-constexpr int KW_U = 4;                      // groups per consumer step
+#ifndef SG_KW_U
+#define SG_KW_U 4
+#endif
+#ifndef SG_KW_SLEEP
+#define SG_KW_SLEEP 200
+#endif
+constexpr int KW_U = SG_KW_U;                // groups per consumer step
 static_assert(WIN_R * 8 * 2 + WIN_WORDS * 16 * 2 <= 196608, "two windows in shared memory");
 
 enum : int { KW_FIRST = 1, KW_LAST = 2, KW_END = 4 };
@@ -1759,7 +1770,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         : "r"(a), "r"(parity)
         : "memory");
     if (done) break;
-    __nanosleep(200);
+    __nanosleep(SG_KW_SLEEP);
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
@@ -2186,32 +2197,14 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
           j = __shfl_sync(SG_FULL, j, 0);
           if ((int)j >= nh) break;
           const int hend = min((int)j + 128, nh);
-          for (int h0 = (int)j; h0 < hend; h0 += 32) {
-            const int h = h0 + lane;
-            uint2 p = make_uint2(0u, 0u);
-            if (h < hend) p = lds_u2(bmw + (uint32_t)h * 8u);
-            const int mx = (int)__reduce_max_sync(SG_FULL, (unsigned)__popc(p.x));
-            if (mx <= 6) {
-              // sparse half-words: each lane writes its few columns (the
-              // lanes' ranges are adjacent, so the stores are near-coalesced)
-              unsigned bits = p.x;
-              int32_t* o = oc + p.y;
-              const int32_t cb = c0 + 32 * h;
-              while (bits) {
-                st_stream(o++, cb + __ffs(bits) - 1);
-                bits &= bits - 1;
-              }
-            } else {
-              // dense: the warp writes one half-word at a time, lane = bit,
-              // one coalesced store of up to 32 columns each
-              const unsigned below = (1u << lane) - 1u;
-              for (int q = 0; q < 32; ++q) {
-                const unsigned bits = __shfl_sync(SG_FULL, p.x, q);
-                if (!bits) continue;
-                const unsigned r = __shfl_sync(SG_FULL, p.y, q);
-                if (bits >> lane & 1u)
-                  st_stream(oc + r + __popc(bits & below), c0 + 32 * (h0 + q) + lane);
-              }
+          for (int h = (int)j + lane; h < hend; h += 32) {
+            const uint2 p = lds_u2(bmw + (uint32_t)h * 8u);
+            unsigned bits = p.x;
+            int32_t* o = oc + p.y;
+            const int32_t cb = c0 + 32 * h;
+            while (bits) {
+              st_stream(o++, cb + __ffs(bits) - 1);
+              bits &= bits - 1;
             }
           }
         }

@@ -211,7 +211,11 @@ SHORT_ROW_ESCR = 512
 BITMAP_SAVE_SHARE = 0.35
 
 
-def windows(ctx: _Ctx, m, products, lo, hi, select) -> Windows:
+def windows(ctx: _Ctx, m, products, lo, hi, select, c_bytes: int = 0) -> Windows:
+    """Window tables of the long rows; their key bitmaps are saved (16 B per
+    64 columns) only when they fit next to `c_bytes` -- the C arrays still to
+    be allocated -- so that C never has to evict them (an eviction costs the
+    bitmap pass and, call after call, re-mapping tens of GB)."""
     off = ctx.empty(m + 1, torch.int64)
     bm_off = ctx.empty(m + 1, torch.int64)
     totals = (ctypes.c_int64 * 2)()
@@ -228,7 +232,7 @@ def windows(ctx: _Ctx, m, products, lo, hi, select) -> Windows:
         # cudaMemGetInfo, which costs milliseconds under expandable segments
         free = _device_total(ctx.device) - torch.cuda.memory_allocated(ctx.device)
         free += _ARENA.held_bytes(ctx.device)
-        if 16 * words <= BITMAP_SAVE_SHARE * free:
+        if 16 * words <= BITMAP_SAVE_SHARE * free and 16 * words + c_bytes <= 0.96 * free:
             bm_save = _ARENA.take(ctx, words)
     return Windows(off, wins, nwin, bm_off, bm_save, pre_save, total)
 
@@ -534,7 +538,14 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     pred_plan = None
     if kind_wf is WorkflowKind.SYMBOLIC:
         pred = ctx.empty(m, torch.int64)
-        win = windows(ctx, m, products, span_lo, span_hi, None)
+        # C's size for the bitmap budget: products / sampled CR, else the
+        # bound sum(min(products, span)) per row
+        vb = 4 + (8 if dtype == torch.float64 else 4)
+        if cr is not None:
+            c_est = int(total_products / max(1.0, cr[0]) * 1.05)
+        else:
+            c_est = int(torch.minimum(products, span_hi - span_lo + 1).clamp(min=0).sum().item()) if m else 0
+        win = windows(ctx, m, products, span_lo, span_hi, None, vb * c_est)
         # assisted symbolic binning with the conservative
         # sampled CR (predict.py:111-118) when the sample was taken
         assist = 1.0 if (cr is None or not cfg.assisted_symbolic) else max(1.0, cr[1] - 2.0 * cr[2])
@@ -662,7 +673,12 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
         sel = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
         if n_fb:
             sel[fb_rows] = 1
-        win = windows(ctx, m, products, span_lo, span_hi, sel)
+        # C's size: the non-fallback rows' exact counts plus the fallback
+        # rows' predictions (estimates / upper bounds), 5% margin
+        vb = 4 + (8 if dtype == torch.float64 else 4)
+        c_est = int((torch.where(sel.bool(), pred.to(torch.float64), counts.to(torch.float64)).sum().item()
+                     if m else 0) * 1.05)
+        win = windows(ctx, m, products, span_lo, span_hi, sel, vb * c_est)
         if n_fb:
             _lib.call("sg_fallback", 0, n_fb, ptr(fb_rows), n, dcode, *fargs, None, None, None,
                       ptr(counts), win.struct(), ws, wsb, ctx.sp)
