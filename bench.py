@@ -253,7 +253,7 @@ def cpu_baseline(a, b, workers, nblocks=None, budget_s=None, warmup=0, keep=Fals
         t = float(np.mean(secs))
         return {"value": 2.0 * total / t / 1e9, "unit": "GFLOP/s", "cores": workers, "kind": ref.kind,
                 "sample": f"whole matrix, AUTO workflow, mean of {len(secs)} calls ({t:.2f} s each)",
-                "extrapolated_seconds": t, "blocks": [(0, a.nrows)], "outputs": outs}
+                "extrapolated_seconds": t, "blocks": [(0, a.nrows)], "outputs": outs, "total_products": total}
     blocks = matgen.stratified_blocks(per)
     t_fixed, wf = ref.fixed(a, b)
     for i in range(warmup):
@@ -282,7 +282,7 @@ def cpu_baseline(a, b, workers, nblocks=None, budget_s=None, warmup=0, keep=Fals
             f"full time = fixed + block time x total / sampled products = {t_full:.1f} s")
     return {"value": 2.0 * total / t_full / 1e9, "unit": "GFLOP/s", "cores": workers, "kind": ref.kind,
             "sample": desc, "workflow": wf, "fixed_seconds": t_fixed, "block_seconds": t_var,
-            "extrapolated_seconds": t_full, "blocks": used, "outputs": outs}
+            "extrapolated_seconds": t_full, "blocks": used, "outputs": outs, "total_products": total}
 
 
 def parity_rows(a, b, c, nblocks):
@@ -404,7 +404,9 @@ def main():
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded generator, SURVEY §8d; values U[0.5,1.5])",
                 "impl": "reference",
-                "config": {"workload": workload, "parallelism": f"cpu threads x{workers}"},
+                "config": {"workload": workload, "m": a.nrows, "k": b.nrows, "n": b.ncols, "nnz_a": a.nnz,
+                           "products": cb.get("total_products"), "parallelism": f"cpu threads x{workers}",
+                           "workflow": cb.get("workflow")},
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)

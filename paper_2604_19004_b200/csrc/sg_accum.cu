@@ -830,6 +830,9 @@ constexpr size_t escr_smem() { return (size_t)ESCR_WARPS * (3 * 33 * 8 + (size_t
 // -------------------------------------------------------------------------
 // HB: block-per-row shared-memory hash
 
+#ifndef SG_HB_RADIX
+#define SG_HB_RADIX 4
+#endif
 template <int LOG2T, int MODE, typename V, int NT>
 __global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* __restrict__ rows, Csr A, Csr B,
                                                    const int8_t* kind, const int64_t* cap, const int64_t* alloc,
@@ -893,7 +896,7 @@ __global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* 
     // values carried along; striped output -> coalesced stores
     {
       constexpr int ITEMS = (T / 2) / NT;
-      using Sorter = cub::BlockRadixSort<uint32_t, NT, ITEMS, double>;
+      using Sorter = cub::BlockRadixSort<uint32_t, NT, ITEMS, double, SG_HB_RADIX>;
       const int32_t lo32 = (int32_t)span_lo[row];
       const uint32_t span = (uint32_t)(span_hi[row] - span_lo[row] + 1);
       const int bits = span <= 1 ? 1 : 32 - __clz(span - 1);
