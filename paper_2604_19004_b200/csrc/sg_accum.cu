@@ -877,20 +877,37 @@ __global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* 
       __syncthreads();
       continue;
     }
-    // in-place ordered compaction, chunks of NT slots
-    int64_t n = 0;
-    for (int s0 = 0; s0 < T; s0 += NT) {
-      const int k = keys[s0 + threadIdx.x];
-      const double v = vals[s0 + threadIdx.x];
-      int64_t tot;
-      const int64_t pos = block_excl_scan((int64_t)(k != -1), scr, &tot);
-      if (k != -1) {
-        keys[n + pos] = k;
-        vals[n + pos] = v;
-      }
-      n += tot;
+    // in-place compaction in any order (the sort below orders it): chunks of
+    // 2*NT slots are read into registers, then (one barrier later) written to
+    // positions from a shared counter, one warp-aggregated atomic per warp;
+    // the writes stay below the chunk's start + the occupied count, so never
+    // reach an unread slot
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    for (int s0 = 0; s0 < T; s0 += 2 * NT) {
+      const int k0 = keys[s0 + threadIdx.x], k1 = (s0 + NT + (int)threadIdx.x < T) ? keys[s0 + NT + threadIdx.x] : -1;
+      const double v0 = vals[s0 + threadIdx.x];
+      const double v1 = (s0 + NT + (int)threadIdx.x < T) ? vals[s0 + NT + threadIdx.x] : 0.0;
       __syncthreads();
+      const unsigned m0 = __ballot_sync(SG_FULL, k0 != -1), m1 = __ballot_sync(SG_FULL, k1 != -1);
+      const int lane = lane_id();
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&cnt, __popc(m0) + __popc(m1));
+      base = __shfl_sync(SG_FULL, base, 0);
+      const unsigned lt = lanemask_lt();
+      if (k0 != -1) {
+        const int p = base + __popc(m0 & lt);
+        keys[p] = k0;
+        vals[p] = v0;
+      }
+      if (k1 != -1) {
+        const int p = base + __popc(m0) + __popc(m1 & lt);
+        keys[p] = k1;
+        vals[p] = v1;
+      }
     }
+    __syncthreads();
+    const int64_t n = cnt;
     // sort the n <= T/2 distinct columns: LSD radix sort (CUB block
     // primitive) on (col - span_lo) over only the bits the row's span needs,
     // values carried along; striped output -> coalesced stores
@@ -1034,6 +1051,8 @@ struct BitmapSetOp {
     atomicOr(reinterpret_cast<unsigned*>(bm) + (x >> 5), 1u << (x & 31));
   }
 };
+
+
 
 template <typename V>
 struct BitmapAddOp {
