@@ -1762,7 +1762,7 @@ struct KwShared {
   int win_done[2];
   unsigned col_next[2];    // column-emission work counter of each window slot
   WinItem items[4];        // producer's work-item ring (loaded two windows ahead)
-  int pscan[KW_PW + 1];
+  int pscan[2][KW_PW + 1];
   int pexcl[KW_NP + 1];
   int64_t ticket;
 };
@@ -1953,22 +1953,45 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
       ch->out_base = it.out_base;
       ch->next = 0;
     }
-    pbar();
-    if (tid == 0) mbar_arrive(&sh.full[cseq % KW_NCH]);
+    // every producer thread arrives once its own table entries are written
+    // (the full barrier counts KW_NP arrivals): no second block barrier
+    mbar_arrive(&sh.full[cseq % KW_NCH]);
     ++cseq;
     KW_ACC(pc_pub);
   };
   // one batch of KW_NP entries into the chunk(s): scan, append, publish full
   // chunks.  (bs, len, a) is this thread's clipped segment.
+  unsigned spar = 0;  // parity of the double-buffered warp totals
   auto append = [&](int64_t bs, int len, double a, int& flags, const WinItem& it, unsigned wslot) {
     KW_T0();
     const int pk = (len << 9) | (len > 0 ? 1 : 0);  // (length, non-empty)
     const int inc = warp_incl_scan(pk);
-    if (lane == 31) sh.pscan[pw] = inc;
+    int* ps = sh.pscan[spar];
+    spar ^= 1u;
+    if (lane == 31) ps[pw] = inc;
     pbar();
-    int wbase = 0;
-    for (int w = 0; w < pw; ++w) wbase += sh.pscan[w];
+    int wbase = 0, btot = 0;
+#pragma unroll
+    for (int w = 0; w < KW_PW; ++w) {
+      const int x = ps[w];
+      wbase += w < pw ? x : 0;
+      btot += x;
+    }
     const int excl = wbase + inc - pk;
+    if (nprod + (btot >> 9) <= KW_PMAX && nseg + (btot & 511) <= KW_SEG) {
+      // common case: the whole batch fits the open chunk -- one barrier
+      if (len > 0) {
+        const int c = nseg + (excl & 511);
+        const int S = nprod + (excl >> 9);
+        ch->S[c] = S;
+        ch->d[c] = bs - S;
+        ch->av[c] = a;
+      }
+      nprod += btot >> 9;
+      nseg += btot & 511;
+      KW_ACC(pc_append);
+      return;
+    }
     sh.pexcl[tid] = excl;
     if (tid == KW_NP - 1) sh.pexcl[KW_NP] = excl + pk;
     pbar();
@@ -2349,7 +2372,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* 
   for (int i = threadIdx.x; i < 2 * WIN_R; i += KW_NT) (&sh.vals[0][0])[i] = 0.0;
   if (threadIdx.x == 0) {
     for (int j = 0; j < KW_NCH; ++j) {
-      mbar_init(&sh.full[j], 1);
+      mbar_init(&sh.full[j], KW_NP);
       mbar_init(&sh.empty[j], KW_CW);
     }
     for (int j = 0; j < 2; ++j) {
