@@ -2322,42 +2322,86 @@ struct LightOp {
   }
 };
 
-template <typename V, int NT>
-__global__ void __launch_bounds__(NT) k_win_light(int64_t m, const int32_t* __restrict__ lcnt, Csr A, Csr B,
-                                                  const int64_t* __restrict__ span_lo,
-                                                  const int64_t* __restrict__ bm_off, const uint4* __restrict__ bm16,
-                                                  const int64_t* __restrict__ row_ptr,
-                                                  const KwEnt* __restrict__ lent, V* __restrict__ out_val) {
+// The light entries' products are combined per row in a shared-memory hash
+// (column -> fp64 sum, open addressing) and the table is flushed -- one RED
+// per distinct column at its row rank -- whenever it could overflow within
+// the next round of entries, and at the row's end.  Hot columns (hub
+// columns receive thousands of light products per dense row) are thereby
+// summed in shared memory instead of serialising at one L2 address.
+constexpr int KL_NT = 512, KL_LOG2T = 13, KL_T = 1 << KL_LOG2T;
+
+template <typename V>
+__global__ void __launch_bounds__(KL_NT, 2) k_win_light(int64_t m, const int32_t* __restrict__ lcnt, Csr A, Csr B,
+                                                        const int64_t* __restrict__ span_lo,
+                                                        const int64_t* __restrict__ bm_off,
+                                                        const uint4* __restrict__ bm16,
+                                                        const int64_t* __restrict__ row_ptr,
+                                                        const KwEnt* __restrict__ lent, V* __restrict__ out_val) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int64_t scr[NT / 32 + 2];
-  Entries E{reinterpret_cast<int64_t*>(smem), reinterpret_cast<int64_t*>(smem) + (NT + 1),
-            reinterpret_cast<double*>(smem) + 2 * (NT + 1)};
+  int* keys = reinterpret_cast<int*>(smem);
+  double* vals = reinterpret_cast<double*>(smem + KL_T * 4);
+  __shared__ int cnt;
+  constexpr int NW = KL_NT / 32;
+  const int w = warp_id(), lane = lane_id();
+  const int32_t* __restrict__ b_col = B.col;
+  const V* __restrict__ b_val = (const V*)B.val;
+  for (int i = threadIdx.x; i < KL_T; i += KL_NT) keys[i] = -1;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
   for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
     const int n = lcnt[row];
     if (n <= 0) continue;
-    LightOp<V> op{reinterpret_cast<const uint2*>(bm16 + bm_off[row]), (int32_t)win_origin(span_lo[row]),
-                  out_val + row_ptr[row]};
+    const uint2* bm = reinterpret_cast<const uint2*>(bm16 + bm_off[row]);
+    const int32_t org = (int32_t)win_origin(span_lo[row]);
+    V* out = out_val + row_ptr[row];
     const KwEnt* le = lent + A.ptr[row];
-    for (int j0 = 0; j0 < n; j0 += NT) {
-      int64_t bs = 0, len = 0;
-      double av = 0.0;
-      if (j0 + (int)threadIdx.x < n) {
-        const KwEnt en = le[j0 + threadIdx.x];
-        bs = en.bs;
-        len = en.len;
-        av = en.av;
+    auto flush = [&]() {
+      __syncthreads();
+      for (int i = threadIdx.x; i < KL_T; i += KL_NT) {
+        const int k = keys[i];
+        if (k != -1) {
+          const uint32_t x = (uint32_t)(k - org);
+          const uint2 q = __ldg(bm + (x >> 5));
+          gmem_red(out + (q.y + __popc(q.x & ((2u << (x & 31)) - 1u)) - 1u), (V)vals[i]);
+          keys[i] = -1;
+        }
       }
-      int64_t tot;
-      const int64_t ex = block_excl_scan((len << 12) | (int64_t)(len > 0), scr, &tot);
-      const int64_t S = ex >> 12, pos = ex & 4095;
-      if (len > 0) {
-        E.S[pos] = S;
-        E.d[pos] = bs - S;
-        E.av[pos] = av;
+      if (threadIdx.x == 0) cnt = 0;
+      __syncthreads();
+    };
+    // rounds of NW entries (one per warp, lanes over its B row: < lh <= 256
+    // products, so a round adds at most NW * 255 keys)
+    for (int j0 = 0; j0 < n; j0 += NW) {
+      if (cnt > 3 * KL_T / 4 - NW * 256) flush();  // keeps the load factor <= 3/4
+      const int j = j0 + w;
+      if (j < n) {
+        const KwEnt en = le[j];
+        for (int q = lane; q < en.len; q += 32) {
+          const int32_t col = __ldg(b_col + en.bs + q);
+          const double v = en.av * (double)__ldg(b_val + en.bs + q);
+          uint32_t s = slot_hash((uint32_t)col, KL_LOG2T);
+          for (;;) {
+            int k = reinterpret_cast<volatile int*>(keys)[s];
+            if (k == -1) {
+              const int old = atomicCAS(&keys[s], -1, col);
+              if (old == -1) {
+                atomicAdd(&cnt, 1);
+                k = col;
+              } else {
+                k = old;
+              }
+            }
+            if (k == col) {
+              smem_add(&vals[s], v);
+              break;
+            }
+            s = (s + 1) & (KL_T - 1);
+          }
+        }
       }
       __syncthreads();
-      block_products<true, V>(E, (int)(tot & 4095), tot >> 12, B.col, (const V*)B.val, op);
     }
+    flush();
   }
 }
 
@@ -3043,7 +3087,7 @@ static int launch_bmr(int64_t n, const WinItem* work, const Csr& A, const Csr& B
 static int light_len() {
   static int v = [] {
     const char* e = getenv("SG_LIGHT_LEN");
-    return e ? atoi(e) : 0;
+    return e ? std::min(atoi(e), 256) : 0;  // k_win_light's table bound assumes < 256 products per entry
   }();
   return v;
 }
@@ -3107,11 +3151,11 @@ static int launch_kwin(int64_t n, const WinItem* work, const Csr& A, const Csr& 
 template <typename V>
 static int launch_light(int64_t m, const Csr& A, const Csr& B, const Win& W, const int64_t* span_lo,
                         const int64_t* row_ptr, const WinScratch& ws, void* out_val, cudaStream_t s) {
-  constexpr int NT = 256;
-  constexpr size_t sm = (size_t)3 * (NT + 1) * 8;
-  auto kern = k_win_light<V, NT>;
+  constexpr int NT = KL_NT;
+  constexpr size_t sm = (size_t)KL_T * 12;
+  auto kern = k_win_light<V>;
   if (int rc = set_smem(kern, sm)) return rc;
-  const int grid = (int)std::min<int64_t>(m, (int64_t)num_sms() * 8);
+  const int grid = (int)std::min<int64_t>(m, (int64_t)num_sms() * 2);
   ktimer_begin("k_win_light", s);
   kern<<<grid, NT, sm, s>>>(m, ws.lcnt, A, B, span_lo, W.bm_off, reinterpret_cast<const uint4*>(W.bm_save), row_ptr,
                             ws.lent, (V*)out_val);
