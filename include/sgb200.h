@@ -178,6 +178,16 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
                       int32_t* out_col, void* out_val, void* work_buf, int64_t work_cap, void* ws,
                       size_t ws_bytes, void* stream);
 
+/* Deterministic values (EngineConfig(deterministic=True)): recomputes every
+ * value of C -- whose structure (c_ptr, c_col, sorted) is final -- as a
+ * sequential sum in the reference's stream order (A entries ascending, then
+ * each B row's entries), one warp per row, no atomics: bit-identical run to
+ * run (the reference's guarantee, engine.py:13-14).  acc: double[nnz(C)]
+ * scratch (may be c_val itself when dtype is f64). */
+int sg_det_values(int64_t m, int dtype, const int64_t* a_ptr, const int32_t* a_col, const void* a_val,
+                  const int64_t* b_ptr, const int32_t* b_col, const void* b_val, const int64_t* c_ptr,
+                  const int32_t* c_col, void* c_val, double* acc, void* stream);
+
 /* Scratch bytes sg_window_numeric needs: window work items plus the heavy /
  * light entry tables of the windowed rows. */
 int64_t sg_window_work_bytes(int64_t m, int64_t nnz_a, int64_t nwindows);

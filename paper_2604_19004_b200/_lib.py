@@ -57,6 +57,7 @@ SIGNATURES = {
                                 I64, P, SZ, P]),
     "sg_btile_plan": (I32, [I64, I64, P, I64, P, P, P, SZ, P]),
     "sg_window_work_bytes": (I64, [I64, I64, I64]),
+    "sg_det_values": (I32, [I64, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "sg_btile_build": (I32, [I64, I64, P, P, P, P, P, P]),
     "sg_plan": (I32, [I64, I32, P, P, P, P, C.POINTER(SgTiers), P, P, P, P]),
     "sg_scan": (I32, [I64, P, P, P, SZ, P]),

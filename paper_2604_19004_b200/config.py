@@ -123,6 +123,10 @@ class EngineConfig:
     # root rank (shard.Decision); a shard then skips its own sampling and
     # reports the global er / cr_hat / workflow / registers
     decision: object | None = None
+    # values summed in the reference's sequential stream order after the
+    # structure is final (sg_det_values): bit-identical run to run, as the
+    # reference guarantees (engine.py:13-14); refbind turns it on
+    deterministic: bool = False
 
     def __post_init__(self):
         if self.registers is not None and self.registers not in PRECISION_FOR:

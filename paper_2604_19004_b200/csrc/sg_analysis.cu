@@ -693,3 +693,72 @@ int sg_compact(int64_t m, int dtype, const int64_t* counts, const uint8_t* skip,
 }
 
 }  // extern "C"
+
+// -------------------------------------------------------------------------
+// Deterministic values (EngineConfig(deterministic=True)): given C's final
+// structure, every value is recomputed as a sum in the reference's stream
+// order -- A entries ascending, then each B row's entries -- with plain
+// adds (no atomics).  One warp per row: the warp walks the row's A entries
+// in order; the lanes of one entry touch distinct C columns (a B row has
+// unique columns), so one entry's adds never collide and the entries are
+// applied one after another.  Values are bit-identical run to run and to a
+// sequential sum (the reference's dense / fallback bins and its oracle,
+// engine.py:13-14, accumulate.py:412-415, oracle.py:28-39).
+namespace sg {
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t* __restrict__ a, int64_t n, int32_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <typename V>
+__global__ void k_det_values(int64_t m, const int64_t* __restrict__ a_ptr, const int32_t* __restrict__ a_col,
+                             const V* __restrict__ a_val, const int64_t* __restrict__ b_ptr,
+                             const int32_t* __restrict__ b_col, const V* __restrict__ b_val,
+                             const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_col,
+                             double* __restrict__ acc, V* __restrict__ c_val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m; r += nwarps) {
+    const int64_t rs = c_ptr[r], n = c_ptr[r + 1] - rs;
+    if (n == 0) continue;
+    double* ar = acc + rs;
+    for (int64_t i = lane; i < n; i += 32) ar[i] = 0.0;
+    __syncwarp();
+    for (int64_t t = a_ptr[r]; t < a_ptr[r + 1]; ++t) {
+      const int32_t k = a_col[t];
+      const double av = (double)a_val[t];
+      const int64_t bs = b_ptr[k], bl = b_ptr[k + 1] - bs;
+      for (int64_t q = lane; q < bl; q += 32) {
+        const int64_t pos = lower_bound_i32(c_col + rs, n, b_col[bs + q]);
+        ar[pos] = __dadd_rn(ar[pos], __dmul_rn(av, (double)b_val[bs + q]));  // no FMA: the reference rounds the product
+      }
+      __syncwarp();
+    }
+    for (int64_t i = lane; i < n; i += 32) c_val[rs + i] = (V)ar[i];
+    __syncwarp();
+  }
+}
+
+}  // namespace sg
+
+extern "C" int sg_det_values(int64_t m, int dtype, const int64_t* a_ptr, const int32_t* a_col, const void* a_val,
+                             const int64_t* b_ptr, const int32_t* b_col, const void* b_val, const int64_t* c_ptr,
+                             const int32_t* c_col, void* c_val, double* acc, void* stream) {
+  using namespace sg;
+  if (m == 0) return SG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int g = (int)std::min<int64_t>((m + 7) / 8, 148 * 64);
+  if (dtype == SG_F64)
+    k_det_values<double><<<g, 256, 0, s>>>(m, a_ptr, a_col, (const double*)a_val, b_ptr, b_col,
+                                           (const double*)b_val, c_ptr, c_col, acc, (double*)c_val);
+  else
+    k_det_values<float><<<g, 256, 0, s>>>(m, a_ptr, a_col, (const float*)a_val, b_ptr, b_col, (const float*)b_val,
+                                          c_ptr, c_col, acc, (float*)c_val);
+  count_launches(1);
+  return check_cuda("k_det_values");
+}

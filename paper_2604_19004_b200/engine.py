@@ -731,6 +731,12 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     if m == 0:
         row_ptr = torch.zeros(1, dtype=torch.int64, device=ctx.device)
         nnz_c = 0
+    if cfg.deterministic and m and nnz_c:
+        # values recomputed in the reference's sequential stream order
+        acc = C_val if C_val.dtype == torch.float64 else ctx.empty(nnz_c, torch.float64)
+        _lib.call("sg_det_values", m, _dtype_code(A.values), *Aargs, ptr(row_ptr), ptr(C_col), ptr(C_val),
+                  ptr(acc), ctx.sp)
+        del acc
     ev[6].record(ctx.stream)
     _nvtx.range_pop()
     ctx.sync()

@@ -33,7 +33,7 @@ _REPORT_FIELDS = None
 def engine_config(ref_cfg) -> _cfg.EngineConfig:
     """The B200 EngineConfig for a reference EngineConfig (or None)."""
     if ref_cfg is None:
-        return _cfg.EngineConfig()
+        return _cfg.EngineConfig(deterministic=True)
     t = ref_cfg.tiers
     tiers = _cfg.TierConfig(hash_capacities=tuple(t.hash_capacities),
                             enhanced_hash_capacity=int(t.enhanced_hash_capacity),
@@ -52,7 +52,10 @@ def engine_config(ref_cfg) -> _cfg.EngineConfig:
         seed=ref_cfg.seed,
         workers=ref_cfg.workers,
         staging_limit_bytes=ref_cfg.staging_limit_bytes,
-        compute_estimation_errors=ref_cfg.compute_estimation_errors)
+        compute_estimation_errors=ref_cfg.compute_estimation_errors,
+        # the reference's contract includes bit-identical values for a fixed
+        # seed at any worker count (engine.py:13-14)
+        deterministic=True)
 
 
 def bind(sg):

@@ -359,3 +359,36 @@ def test_repeat_runs_structure_identical(gpu):
     np.testing.assert_allclose(C1.values, C2.values, rtol=1e-12, atol=0)
     for k in REPORT_EXACT + REPORT_FLOAT:
         assert getattr(r1, k) == getattr(r2, k), k
+
+
+@pytest.mark.parametrize("name", ["pair03", "corpus1", "enhanced", "fig2"])
+def test_deterministic_values_bitwise(gpu, name):
+    """EngineConfig(deterministic=True): values summed in the reference's
+    sequential stream order (sg_det_values) -- bit-identical across runs and
+    workflows, and bit-identical to the sequential dict oracle
+    (oracle.py:28-39); structure as always."""
+    from paper_2604_19004_b200 import EngineConfig, WorkflowOverride, spgemm
+    from oracle import ocean_cpu as oc
+    c = Case(name)
+    seq = oc.dict_spgemm(c.A, c.B)
+    outs = []
+    for o in (WorkflowOverride.AUTO, WorkflowOverride.FORCE_ESTIMATE, WorkflowOverride.FORCE_UPPER_BOUND):
+        C, _ = spgemm(c.A, c.B, EngineConfig(workflow=o, deterministic=True))
+        np.testing.assert_array_equal(C.row_ptr, seq.row_ptr)
+        np.testing.assert_array_equal(C.col_idx, seq.col_idx)
+        np.testing.assert_array_equal(C.values, seq.values)  # bitwise
+        outs.append(C.values)
+    for v in outs[1:]:
+        assert (v == outs[0]).all()
+
+
+def test_deterministic_values_rmat(gpu):
+    """Deterministic mode on hub rows with windows (R-MAT 12): bitwise equal
+    to the sequential oracle."""
+    from paper_2604_19004_b200 import EngineConfig, matgen, spgemm
+    from oracle import ocean_cpu as oc
+    a = matgen.rmat(12, seed=4)
+    seq = oc.dict_spgemm(a, a)
+    C, _ = spgemm(a, a, EngineConfig(deterministic=True))
+    np.testing.assert_array_equal(C.col_idx, seq.col_idx)
+    np.testing.assert_array_equal(C.values, seq.values)
