@@ -831,7 +831,7 @@ constexpr size_t escr_smem() { return (size_t)ESCR_WARPS * (3 * 33 * 8 + (size_t
 // HB: block-per-row shared-memory hash
 
 #ifndef SG_HB_RADIX
-#define SG_HB_RADIX 4
+#define SG_HB_RADIX 5  // 4 passes over the 20 key bits of a 2^20-column span
 #endif
 template <int LOG2T, int MODE, typename V, int NT>
 __global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* __restrict__ rows, Csr A, Csr B,
@@ -916,18 +916,22 @@ __global__ void __launch_bounds__(NT) k_hash_block(int64_t nbin, const int32_t* 
       using Sorter = cub::BlockRadixSort<uint32_t, NT, ITEMS, double, SG_HB_RADIX>;
       const int32_t lo32 = (int32_t)span_lo[row];
       const uint32_t span = (uint32_t)(span_hi[row] - span_lo[row] + 1);
+      static_assert(sizeof(typename Sorter::TempStorage) <= ((size_t)1 << LOG2T) * 12, "sort storage");
+      // keys < 2^bits; the padding items (blocked positions >= n) take the
+      // largest key, and the stable sort keeps them after the n real ones
       const int bits = span <= 1 ? 1 : 32 - __clz(span - 1);
+      const uint32_t pad = bits < 32 ? (1u << bits) - 1u : 0xffffffffu;
       uint32_t kk[ITEMS];
       double vv[ITEMS];
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
         const int idx = threadIdx.x * ITEMS + i;
-        kk[i] = idx < n ? (uint32_t)(keys[idx] - lo32) : 0xffffffffu;
+        kk[i] = idx < n ? (uint32_t)(keys[idx] - lo32) : pad;
         vv[i] = idx < n ? vals[idx] : 0.0;
       }
       __syncthreads();
       auto& tmp = *reinterpret_cast<typename Sorter::TempStorage*>(smem);
-      Sorter(tmp).SortBlockedToStriped(kk, vv, 0, bits < 32 ? bits + 1 : 32);
+      Sorter(tmp).SortBlockedToStriped(kk, vv, 0, bits);
       const int64_t off = out_off[row];
 #pragma unroll
       for (int i = 0; i < ITEMS; ++i) {
