@@ -230,9 +230,9 @@ __device__ __forceinline__ double lds_f64(uint32_t a) {
 template <bool VALUES, typename V, class Op>
 __device__ __forceinline__ void block_products(const Entries& E, int nent, int64_t P,
                                                const int32_t* __restrict__ b_col,
-                                               const V* __restrict__ b_val, Op& op) {
-  int2* grp = g_grp;
-  const uint32_t grp_s = smem_u32(g_grp), d_s = smem_u32(E.d), av_s = smem_u32(E.av);
+                                               const V* __restrict__ b_val, Op& op, int2* grp = g_grp,
+                                               int grp_max = GRP_MAX) {
+  const uint32_t grp_s = smem_u32(grp), d_s = smem_u32(E.d), av_s = smem_u32(E.av);
   const int nw = blockDim.x >> 5, w = warp_id(), lane = lane_id();
   const unsigned le = lanemask_le();
 #ifndef SG_UNR_KEYS
@@ -241,8 +241,8 @@ __device__ __forceinline__ void block_products(const Entries& E, int nent, int64
   // key passes carry a column per product (values passes a column and a
   // value): twice the gathers in flight at the same register budget
   constexpr int U = VALUES ? SG_UNR : SG_UNR_KEYS;
-  for (int64_t base = 0; base < P; base += 32 * (int64_t)GRP_MAX) {
-    const int rem = (int)min((int64_t)32 * GRP_MAX, P - base);  // products of this sub-chunk
+  for (int64_t base = 0; base < P; base += 32 * (int64_t)grp_max) {
+    const int rem = (int)min((int64_t)32 * grp_max, P - base);  // products of this sub-chunk
     const int ng = (rem + 31) >> 5;
     for (int g = threadIdx.x; g < ng; g += blockDim.x) {
       const int64_t q = base + 32 * (int64_t)g;
@@ -356,7 +356,8 @@ __device__ __forceinline__ void block_row(int64_t row, const int64_t* __restrict
                                           const int32_t* __restrict__ a_col, const V* __restrict__ a_val,
                                           const int64_t* __restrict__ b_ptr, const int32_t* __restrict__ b_col,
                                           const V* __restrict__ b_val, Entries E, int64_t* scan_scratch,
-                                          Op& op, volatile int* stop, int64_t max_len = NOLIMIT) {
+                                          Op& op, volatile int* stop, int64_t max_len = NOLIMIT,
+                                          int2* grp = g_grp, int grp_max = GRP_MAX) {
   const int nw = blockDim.x >> 5, w = warp_id();
   const int64_t t1 = a_ptr[row + 1];
   for (int64_t t = a_ptr[row]; t < t1; t += blockDim.x) {
@@ -382,7 +383,7 @@ __device__ __forceinline__ void block_row(int64_t row, const int64_t* __restrict
 #if SG_GROUPED
     (void)nw;
     (void)w;
-    block_products<VALUES, V>(E, (int)nent64, P, b_col, b_val, op);
+    block_products<VALUES, V>(E, (int)nent64, P, b_col, b_val, op, grp, grp_max);
 #else
     const int64_t per = ((P + nw - 1) / nw + 31) & ~(int64_t)31;
     const int64_t pb = min(P, per * w), pe = min(P, per * (w + 1));
@@ -1197,6 +1198,18 @@ __device__ __forceinline__ int64_t prefix_save(const unsigned long long* bm, int
   return tot;
 }
 
+// k_bitmap shared layout: bitmap (BW words) | ranks | [group table] | entries.
+// MODE 1 ranks every word; MODE 0 only the 4096-column tiles.
+template <int BW, int MODE>
+__host__ __device__ constexpr size_t bm_pre_bytes() {
+  return MODE == 0 ? (((size_t)BW / TILE_WORDS * 4 + 15) & ~(size_t)15) : (size_t)BW * 4;
+}
+// own group table (groups) of the long-row count pass; 0: the shared g_grp
+template <int BW, int MODE>
+__host__ __device__ constexpr int bm_grp() {
+  return (MODE == 0 && BW >= 16384) ? 4096 : 0;
+}
+
 template <int BW, int MODE, typename V, int NT>
 __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __restrict__ rows, Csr A, Csr B,
                                                const int8_t* kind, const int64_t* cap, const int64_t* alloc,
@@ -1211,9 +1224,16 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
   int32_t* __restrict__ nwin = win.nwin;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int64_t scr[NT / 32 + 2];
+  // MODE 0 keeps only tile ranks (not word ranks); the long-row count pass
+  // has its own group table of bm_grp() groups in dynamic shared memory, so
+  // a long row's products run in sub-chunks of 32 * 4096 between barriers
+  constexpr int OWN = bm_grp<BW, MODE>();
+  constexpr size_t PRE = bm_pre_bytes<BW, MODE>();
   unsigned long long* bm = reinterpret_cast<unsigned long long*>(smem);
   int* pre = reinterpret_cast<int*>(smem + (size_t)BW * 8);
-  unsigned char* ebase = smem + (size_t)BW * 12;
+  int2* grp = OWN ? reinterpret_cast<int2*>(smem + (size_t)BW * 8 + PRE) : g_grp;
+  constexpr int GRP = OWN ? OWN : GRP_MAX;
+  unsigned char* ebase = smem + (size_t)BW * 8 + PRE + (size_t)OWN * 8;
   Entries E{reinterpret_cast<int64_t*>(ebase), reinterpret_cast<int64_t*>(ebase) + (NT + 1),
             reinterpret_cast<double*>(ebase) + 2 * (NT + 1)};
   constexpr int64_t WCOLS = (int64_t)BW * 64;
@@ -1266,7 +1286,8 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
       for (int i = threadIdx.x; i < nwords; i += NT) bm[i] = 0ull;
       __syncthreads();
       BitmapSetOp<V> so{bm, (int32_t)wlo, (uint32_t)(whi - wlo)};
-      block_row<false, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, so, nullptr);
+      block_row<false, V>(row, A.ptr, A.col, (const V*)A.val, B.ptr, B.col, (const V*)B.val, E, scr, so, nullptr,
+                          NOLIMIT, grp, GRP);
       if (MODE == 0 && wcap == 0) {
         int64_t c = 0;
         for (int i = threadIdx.x; i < nwords; i += NT) c += __popcll(bm[i]);
@@ -1363,9 +1384,9 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
   }
 }
 
-template <int BW, int NT>
+template <int BW, int MODE, int NT>
 constexpr size_t bm_smem() {
-  return (size_t)BW * 12 + (size_t)3 * (NT + 1) * 8;
+  return (size_t)BW * 8 + bm_pre_bytes<BW, MODE>() + (size_t)bm_grp<BW, MODE>() * 8 + (size_t)3 * (NT + 1) * 8;
 }
 
 // -------------------------------------------------------------------------
@@ -2932,7 +2953,7 @@ static int launch_hb(const Launch& L, const int32_t* rows, int64_t n) {
 
 template <int BW, int MODE, typename V, int NT>
 static int launch_bm(const Launch& L, const int32_t* rows, int64_t n) {
-  constexpr size_t sm = bm_smem<BW, NT>();
+  constexpr size_t sm = bm_smem<BW, MODE, NT>();
   auto kern = k_bitmap<BW, MODE, V, NT>;
   if (int rc = set_smem(kern, sm)) return rc;
   int g = (int)std::min<int64_t>(n, (int64_t)num_sms() * 32);
