@@ -1205,9 +1205,12 @@ __host__ __device__ constexpr size_t bm_pre_bytes() {
   return MODE == 0 ? (((size_t)BW / TILE_WORDS * 4 + 15) & ~(size_t)15) : (size_t)BW * 4;
 }
 // own group table (groups) of the long-row count pass; 0: the shared g_grp
+#ifndef SG_BM0_GRP
+#define SG_BM0_GRP 4096
+#endif
 template <int BW, int MODE>
 __host__ __device__ constexpr int bm_grp() {
-  return (MODE == 0 && BW >= 16384) ? 4096 : 0;
+  return (MODE == 0 && BW >= 16384) ? SG_BM0_GRP : 0;
 }
 
 template <int BW, int MODE, typename V, int NT>
@@ -1779,8 +1782,15 @@ struct KwChunk {
   uint32_t next;           // consumer step counter
 };
 
+// fp64 window values leave through a bulk shared->global copy and are
+// re-zeroed by a bulk copy from this zero buffer: a slot holds WIN_R values
+// from element 0 or 1 (C's first value's address mod 16), so the body of the
+// copy is 16-byte aligned on both sides
+constexpr int KW_VSLOT = WIN_R + 2;
+__device__ __align__(16) double g_kw_zero[KW_VSLOT];
+
 struct KwShared {
-  double vals[2][WIN_R];
+  double vals[2][KW_VSLOT];
   uint4 bm[2][WIN_WORDS];
   KwChunk ch[KW_NCH];
   unsigned long long full[KW_NCH], empty[KW_NCH], bm_full[2], win_free[2];
@@ -1825,6 +1835,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\n\tcp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void pbar() { asm volatile("bar.sync 1, %0;" ::"n"(KW_NP) : "memory"); }
 __device__ __forceinline__ int pbar_popc(bool p) {
@@ -1940,8 +1961,11 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
       KW_ACC(pc_free);
       if (tid == 0) {
         const unsigned nwords = (unsigned)(((int64_t)copy_item->c1 - copy_item->c0 + 63) >> 6);
-        mbar_arrive_tx(&sh.bm_full[copy_slot], nwords * 16u);
+        // fp64: the slot's values [0, shift + cnt) re-zeroed by the copy engine
+        const unsigned zb = sizeof(V) == 8 ? ((1u + (unsigned)copy_item->cnt) * 8u + 15u) & ~15u : 0u;
+        mbar_arrive_tx(&sh.bm_full[copy_slot], nwords * 16u + zb);
         bulk_g2s(&sh.bm[copy_slot][0], bm16 + copy_item->bm_word, nwords * 16u, &sh.bm_full[copy_slot]);
+        if (zb) bulk_g2s(&sh.vals[copy_slot][0], g_kw_zero, zb, &sh.bm_full[copy_slot]);
       }
       copy_pending = false;
     }
@@ -2204,7 +2228,9 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
 #ifdef SG_PROF
     const long long _kg = clock64();
 #endif
-    WinAddOp op{smem_u32(&sh.bm[ws][0]), smem_u32(&sh.vals[ws][0]) - (uint32_t)rank0 * 8u, c0};
+    // (see KW_VSLOT) values from slot element 1 when C's first value is not 16-byte aligned
+    const uint32_t vshift = sizeof(V) == 8 ? (uint32_t)((reinterpret_cast<uintptr_t>(out_val + out_base) >> 3) & 1u) : 0u;
+    WinAddOp op{smem_u32(&sh.bm[ws][0]), smem_u32(&sh.vals[ws][0]) + (vshift - (uint32_t)rank0) * 8u, c0};
     const uint32_t grp_s = smem_u32(&ch.grp[0]), d_s = smem_u32(&ch.d[0]), av_s = smem_u32(&ch.av[0]);
     for (;;) {
       unsigned g0 = 0;
@@ -2281,6 +2307,7 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
       }
       KW_ACC(cc_col);
       __threadfence_block();
+      if (sizeof(V) == 8) fence_proxy_async_smem();  // this warp's value adds -> the bulk store
       int n = 0;
       if (lane == 0) n = atomicAdd(&sh.win_done[ws], 1);
       n = __shfl_sync(SG_FULL, n, 0);
@@ -2290,6 +2317,20 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
         // and zero them for the window after next
         const uint32_t vs = smem_u32(&sh.vals[ws][0]);
         V* dst = out_val + out_base;
+        if constexpr (sizeof(V) == 8) {
+          // one bulk copy of the 16-byte aligned body (the producer re-zeroes
+          // the slot with its next bitmap copy), head / tail element apart
+          if (lane == 0) {
+            const int head = (int)vshift < cnt ? (int)vshift : 0;
+            const int body = (cnt - head) & ~1;
+            if (head) st_stream(dst, (V)lds_f64(vs + 8u));
+            if (head + body < cnt) st_stream(dst + head + body, (V)lds_f64(vs + (vshift + head + body) * 8u));
+            if (body > 0) {
+              bulk_s2g(dst + head, vs + (vshift + head) * 8u, (unsigned)body * 8u);
+              bulk_commit_wait_read();  // the slot may be re-zeroed once read
+            }
+          }
+        } else {
         int i = lane;
         for (; i + 96 < cnt; i += 128) {
           const double x0 = lds_f64(vs + i * 8u), x1 = lds_f64(vs + (i + 32) * 8u);
@@ -2307,6 +2348,7 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
           st_stream(dst + i, (V)lds_f64(vs + i * 8u));
           sts_f64(vs + i * 8u, 0.0);
         }
+        }
         __syncwarp();
         if (lane == 0) {
           sh.win_done[ws] = 0;
@@ -2318,6 +2360,7 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
     }
     ++cseq;
   }
+  if (sizeof(V) == 8 && lane == 0) bulk_wait_all();  // value stores complete before exit
 #ifdef SG_PROF
   if (lane == 0) {
     atomicAdd(&g_kw[8], cc_full);
@@ -2438,7 +2481,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* 
                                                   int kw_skip) {
   extern __shared__ __align__(128) unsigned char kw_smem[];
   KwShared& sh = *reinterpret_cast<KwShared*>(kw_smem);
-  for (int i = threadIdx.x; i < 2 * WIN_R; i += KW_NT) (&sh.vals[0][0])[i] = 0.0;
+  for (int i = threadIdx.x; i < 2 * KW_VSLOT; i += KW_NT) (&sh.vals[0][0])[i] = 0.0;
   if (threadIdx.x == 0) {
     for (int j = 0; j < KW_NCH; ++j) {
       mbar_init(&sh.full[j], KW_NP);
