@@ -668,20 +668,23 @@ def _spgemm(a, b, cfg, deadline, ctx: _Ctx):
     fargs = (*Aargs, ptr(products), ptr(span_lo), ptr(span_hi))
     if exact:
         C_col, C_val = out_col, out_val
+    elif not n_fb:
+        # no fallback rows: the numeric counts are final (no windows)
+        row_ptr = scan(ctx, counts)
+        nnz_c = int(row_ptr[-1].item()) if m else 0
+        C_col, C_val = alloc_c(ctx, nnz_c, dtype, None)
     else:
         # count the fallback rows (recording windows for long ones), size C
         sel = torch.zeros(m, dtype=torch.uint8, device=ctx.device)
-        if n_fb:
-            sel[fb_rows] = 1
+        sel[fb_rows] = 1
         # C's size: the non-fallback rows' exact counts plus the fallback
         # rows' predictions (estimates / upper bounds), 5% margin
         vb = 4 + (8 if dtype == torch.float64 else 4)
         c_est = int((torch.where(sel.bool(), pred.to(torch.float64), counts.to(torch.float64)).sum().item()
                      if m else 0) * 1.05)
         win = windows(ctx, m, products, span_lo, span_hi, sel, vb * c_est)
-        if n_fb:
-            _lib.call("sg_fallback", 0, n_fb, ptr(fb_rows), n, dcode, *fargs, None, None, None,
-                      ptr(counts), win.struct(), ws, wsb, ctx.sp)
+        _lib.call("sg_fallback", 0, n_fb, ptr(fb_rows), n, dcode, *fargs, None, None, None,
+                  ptr(counts), win.struct(), ws, wsb, ctx.sp)
         row_ptr = scan(ctx, counts)
         nnz_c = int(row_ptr[-1].item()) if m else 0
         C_col, C_val = alloc_c(ctx, nnz_c, dtype, win)
