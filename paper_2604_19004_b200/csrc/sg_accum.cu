@@ -1793,8 +1793,10 @@ struct KwShared {
   double vals[2][KW_VSLOT];
   uint4 bm[2][WIN_WORDS];
   KwChunk ch[KW_NCH];
-  unsigned long long full[KW_NCH], empty[KW_NCH], bm_full[2], win_free[2];
-  int win_done[2];
+  // win_done[s]: every consumer thread arrives once it is done with the
+  // slot's window (products and column emission); the producer then stores
+  // the window's values and loads the slot's next window
+  unsigned long long full[KW_NCH], empty[KW_NCH], bm_full[2], win_done[2];
   unsigned col_next[2];    // column-emission work counter of each window slot
   WinItem items[4];        // producer's work-item ring (loaded two windows ahead)
   int pscan[2][KW_PW + 1];
@@ -1928,11 +1930,41 @@ __device__ __forceinline__ void kw_clip(const KwEnt& en, const int32_t* __restri
   len = (int)(ee - ss);
 }
 
+// Store the values of the window that held slot ws (all consumer warps have
+// arrived on win_done[ws]) and leave the slot zeroed (float) or to be zeroed
+// by the next bulk load (fp64).  fp64: tid 0 hands them to the copy engine --
+// one bulk shared->global copy of the 16-byte aligned body, head / tail
+// element apart -- and waits until the copy has read the slot.
+template <typename V>
+__device__ __forceinline__ void kw_store_window(KwShared& sh, unsigned ws, V* __restrict__ out_val,
+                                                int64_t out_base, int cnt, int tid) {
+  const uint32_t vs = smem_u32(&sh.vals[ws][0]);
+  V* dst = out_val + out_base;
+  if constexpr (sizeof(V) == 8) {
+    if (tid == 0) {
+      const uint32_t vshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst) >> 3) & 1u);  // see KW_VSLOT
+      const int head = (int)vshift < cnt ? (int)vshift : 0;
+      const int body = (cnt - head) & ~1;
+      if (head) st_stream(dst, (V)lds_f64(vs + 8u));
+      if (head + body < cnt) st_stream(dst + head + body, (V)lds_f64(vs + (vshift + head + body) * 8u));
+      if (body > 0) {
+        bulk_s2g(dst + head, vs + (vshift + head) * 8u, (unsigned)body * 8u);
+        bulk_commit_wait_read();  // the slot may be re-zeroed once read
+      }
+    }
+  } else {
+    for (int i = tid; i < cnt; i += KW_NP) {
+      st_stream(dst + i, (V)lds_f64(vs + i * 8u));
+      sts_f64(vs + i * 8u, 0.0);
+    }
+  }
+}
+
 template <typename V>
 __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const WinItem* __restrict__ work,
                                             const Csr& A, const Csr& B, const BTile& bt,
                                             const uint4* __restrict__ bm16, const KwEnt* __restrict__ hent,
-                                            unsigned long long* ticket) {
+                                            V* __restrict__ out_val, unsigned long long* ticket) {
   (void)A;
   (void)ticket;
   const int tid = threadIdx.x;  // 0 .. KW_NP-1
@@ -1954,12 +1986,24 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   bool copy_pending = false;
   const WinItem* copy_item = nullptr;
   unsigned copy_slot = 0, copy_wseq = 0;
+  int64_t prev_base[2] = {0, 0};  // C offset / values of the window last loaded into each slot
+  int prev_cnt[2] = {0, 0};
+  // wait until the consumers are done with the window in slot ws (its u-th
+  // use), then store its values
+  auto release = [&](unsigned ws, unsigned u) {
+    mbar_wait(&sh.win_done[ws], u & 1u);
+    kw_store_window<V>(sh, ws, out_val, prev_base[ws], prev_cnt[ws], tid);
+    if (sizeof(V) != 8) pbar();
+  };
   auto publish = [&](int flags, const WinItem& it, unsigned wslot) {
     if (copy_pending) {
       KW_T0();
-      mbar_wait(&sh.win_free[copy_slot], ((copy_wseq >> 1) & 1u) ^ 1u);
+      if (copy_wseq >= 2) release(copy_slot, (copy_wseq >> 1) - 1u);
       KW_ACC(pc_free);
+      prev_base[copy_slot] = copy_item->out_base;
+      prev_cnt[copy_slot] = copy_item->cnt;
       if (tid == 0) {
+        sh.col_next[copy_slot] = 0;
         const unsigned nwords = (unsigned)(((int64_t)copy_item->c1 - copy_item->c0 + 63) >> 6);
         // fp64: the slot's values [0, shift + cnt) re-zeroed by the copy engine
         const unsigned zb = sizeof(V) == 8 ? ((1u + (unsigned)copy_item->cnt) * 8u + 15u) & ~15u : 0u;
@@ -2183,6 +2227,9 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   acquire();
   WinItem none{};
   publish(KW_END, none, 0);
+  // the last window of each slot
+  for (unsigned w = wseq >= 2 ? wseq - 2 : 0; w < wseq; ++w) release(w & 1u, w >> 1);
+  if (sizeof(V) == 8 && tid == 0) bulk_wait_all();  // value stores complete before exit
 #ifdef SG_PROF
   if (tid == 0) {
     atomicAdd(&g_kw[0], pc_free);
@@ -2307,60 +2354,12 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
       }
       KW_ACC(cc_col);
       __threadfence_block();
-      if (sizeof(V) == 8) fence_proxy_async_smem();  // this warp's value adds -> the bulk store
-      int n = 0;
-      if (lane == 0) n = atomicAdd(&sh.win_done[ws], 1);
-      n = __shfl_sync(SG_FULL, n, 0);
-      if (n == KW_CW - 1) {
-        KW_T0();
-        // last warp out: store the window's values (coalesced, streaming)
-        // and zero them for the window after next
-        const uint32_t vs = smem_u32(&sh.vals[ws][0]);
-        V* dst = out_val + out_base;
-        if constexpr (sizeof(V) == 8) {
-          // one bulk copy of the 16-byte aligned body (the producer re-zeroes
-          // the slot with its next bitmap copy), head / tail element apart
-          if (lane == 0) {
-            const int head = (int)vshift < cnt ? (int)vshift : 0;
-            const int body = (cnt - head) & ~1;
-            if (head) st_stream(dst, (V)lds_f64(vs + 8u));
-            if (head + body < cnt) st_stream(dst + head + body, (V)lds_f64(vs + (vshift + head + body) * 8u));
-            if (body > 0) {
-              bulk_s2g(dst + head, vs + (vshift + head) * 8u, (unsigned)body * 8u);
-              bulk_commit_wait_read();  // the slot may be re-zeroed once read
-            }
-          }
-        } else {
-        int i = lane;
-        for (; i + 96 < cnt; i += 128) {
-          const double x0 = lds_f64(vs + i * 8u), x1 = lds_f64(vs + (i + 32) * 8u);
-          const double x2 = lds_f64(vs + (i + 64) * 8u), x3 = lds_f64(vs + (i + 96) * 8u);
-          st_stream(dst + i, (V)x0);
-          st_stream(dst + i + 32, (V)x1);
-          st_stream(dst + i + 64, (V)x2);
-          st_stream(dst + i + 96, (V)x3);
-          sts_f64(vs + i * 8u, 0.0);
-          sts_f64(vs + (i + 32) * 8u, 0.0);
-          sts_f64(vs + (i + 64) * 8u, 0.0);
-          sts_f64(vs + (i + 96) * 8u, 0.0);
-        }
-        for (; i < cnt; i += 32) {
-          st_stream(dst + i, (V)lds_f64(vs + i * 8u));
-          sts_f64(vs + i * 8u, 0.0);
-        }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          sh.win_done[ws] = 0;
-          sh.col_next[ws] = 0;
-          mbar_arrive(&sh.win_free[ws]);
-        }
-        KW_ACC(cc_store);
-      }
+      fence_proxy_async_smem();  // this warp's bitmap reads / value adds -> the bulk copies
+      mbar_arrive(&sh.win_done[ws]);  // every lane: its own reads are ordered before the release
+      KW_ACC(cc_store);
     }
     ++cseq;
   }
-  if (sizeof(V) == 8 && lane == 0) bulk_wait_all();  // value stores complete before exit
 #ifdef SG_PROF
   if (lane == 0) {
     atomicAdd(&g_kw[8], cc_full);
@@ -2489,15 +2488,14 @@ __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* 
     }
     for (int j = 0; j < 2; ++j) {
       mbar_init(&sh.bm_full[j], 1);
-      mbar_init(&sh.win_free[j], 1);
-      sh.win_done[j] = 0;
+      mbar_init(&sh.win_done[j], KW_CW * 32);
       sh.col_next[j] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (warp_id() < KW_PW)
-    kw_producer<V>(sh, nwork, work, A, B, bt, bm16, hent, ticket);
+    kw_producer<V>(sh, nwork, work, A, B, bt, bm16, hent, out_val, ticket);
   else
     kw_consumer<V>(sh, B, out_col, out_val, kw_skip);
 }
@@ -3320,6 +3318,12 @@ int sg_fallback(int mode, int64_t nrows, const int64_t* rows, int64_t b_ncols, i
            out_off, out_col, out_val, counts, nullptr, s};
   L.b_ncols = b_ncols;
   if (mode == 0) L.win = to_win(win);
+  if (getenv("SG_PRINT_BINS")) {  // analysis hook: rows per accumulator bin
+    fprintf(stderr, "fallback bins(mode %d):", mode);
+    for (int b = 0; b < NBINS; ++b)
+      if (cnt[b]) fprintf(stderr, " %d:%lld", b, (long long)cnt[b]);
+    fprintf(stderr, "\n");
+  }
   int nonempty = 0;
   for (int b : kOrder) nonempty += cnt[b] != 0;
   Fork f(s);

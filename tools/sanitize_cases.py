@@ -28,7 +28,10 @@ def check(c, ref):
 
 def main():
     n = 0
-    for name in ("fig2", "pair00", "pair05", "corpus1", "enhanced", "tiny_tiers", "bitmapq"):
+    # SANITIZE_ONLY=stress: only the stress shapes (the window kernels)
+    only = os.environ.get("SANITIZE_ONLY")
+    for name in (() if only == "stress" else ("fig2", "pair00", "pair05", "corpus1", "enhanced", "tiny_tiers",
+                                              "bitmapq")):
         cs = Case(name)
         for o in OVR:
             c, _ = spgemm(cs.A, cs.B, EngineConfig(workflow=o, tiers=cs.tiers() or EngineConfig().tiers))
@@ -42,6 +45,9 @@ def main():
             c, _ = spgemm(a, b, EngineConfig(workflow=o))
             check(c, ref)
             n += 1
+    if only == "stress":
+        print(f"sanitize cases ok: {n} multiplies checked")
+        return
     a = matgen.rmat(11, seed=5)
     ref, _ = oc.spgemm(a, a)
     engine.BITMAP_SAVE_SHARE = 0.0  # window pass rebuilding keys itself
