@@ -1121,13 +1121,18 @@ __device__ __forceinline__ void emit_bits(unsigned long long bits, int32_t colba
 // the window accumulator): a window holds at most WIN_R distinct columns and
 // spans at most WIN_WORDS*64 columns, so its bitmap, rank prefix and values
 // all sit in shared memory.
-constexpr int WIN_WORDS = 2048;  // 131,072 columns
-constexpr int WIN_R = 8192;      // values per window (64 KB fp64: two windows in flight per SM)
+#ifndef SG_WIN_WORDS
+#define SG_WIN_WORDS 2048
+#endif
+constexpr int WIN_WORDS = SG_WIN_WORDS;  // 2048: 131,072 columns
+#ifndef SG_WIN_R
+#define SG_WIN_R 8192
+#endif
+constexpr int WIN_R = SG_WIN_R;  // values per window (8192: 64 KB fp64, two windows in flight per SM)
 // Windows start on TILE_COLS-column tiles (absolute), so each selected B
 // row's segment in a window is two lookups in the B tile index (no search).
 constexpr int TILE_COLS = 4096;
 constexpr int TILE_WORDS = TILE_COLS / 64;
-constexpr int WIN_RP = WIN_R - TILE_COLS;  // a tile adds at most TILE_COLS keys
 constexpr int WIN_TILES = WIN_WORDS / TILE_WORDS;
 constexpr int WIN_NT = 1024;
 
@@ -1158,7 +1163,8 @@ __host__ __device__ __forceinline__ bool count_uses_bitmap(int64_t p, int64_t sp
 __host__ __device__ __forceinline__ int64_t window_capacity(int64_t products, int64_t span) {
   if (products <= 0 || span <= 0) return 0;
   const int64_t d = products < span ? products : span;
-  return d / WIN_RP + (span + TILE_COLS) / TILE_COLS / WIN_TILES + 2;
+  // two consecutive windows cut by the WIN_R rule hold > WIN_R keys together
+  return 2 * d / WIN_R + (span + TILE_COLS) / TILE_COLS / WIN_TILES + 3;
 }
 
 // Count pass of a windowed row (one sweep): word ranks, the saved 16-byte
@@ -1309,10 +1315,8 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
                                       pre, scr)
                     : bitmap_prefix<NT>(bm, pre, nwords, scr);
       if (MODE == 0) {
-        // emit numeric windows.  Tile t (TILE_WORDS words, relative to the
-        // tile-aligned origin) belongs to window id = rank(t)/WIN_RP +
-        // t/WIN_TILES with rank(t) the row rank of the tile's first column;
-        // a window starts at every tile whose id differs from the previous.
+        // emit numeric windows (tiles of TILE_WORDS words from the
+        // tile-aligned origin):
         const int64_t gw0 = (wlo - org) >> 6;  // count windows are tile-aligned
         int2* wrow = wins + win_off[row];
         // (the row's bitmap was saved by prefix_save with the row rank of
@@ -1768,7 +1772,6 @@ constexpr int KW_PMAX = 32 * KW_GRP;         // products per chunk
 #define SG_KW_SLEEP 200
 #endif
 constexpr int KW_U = SG_KW_U;                // groups per consumer step
-static_assert(WIN_R * 8 * 2 + WIN_WORDS * 16 * 2 <= 196608, "two windows in shared memory");
 
 enum : int { KW_FIRST = 1, KW_LAST = 2, KW_END = 4 };
 
@@ -1787,22 +1790,28 @@ struct KwChunk {
 // from element 0 or 1 (C's first value's address mod 16), so the body of the
 // copy is 16-byte aligned on both sides
 constexpr int KW_VSLOT = WIN_R + 2;
+#ifndef SG_KW_NWS
+#define SG_KW_NWS 2
+#endif
+constexpr int KW_NWS = SG_KW_NWS;  // window slots in flight per CTA
 __device__ __align__(16) double g_kw_zero[KW_VSLOT];
 
 struct KwShared {
-  double vals[2][KW_VSLOT];
-  uint4 bm[2][WIN_WORDS];
+  double vals[KW_NWS][KW_VSLOT];
+  uint4 bm[KW_NWS][WIN_WORDS];
   KwChunk ch[KW_NCH];
   // win_done[s]: every consumer thread arrives once it is done with the
   // slot's window (products and column emission); the producer then stores
   // the window's values and loads the slot's next window
-  unsigned long long full[KW_NCH], empty[KW_NCH], bm_full[2], win_done[2];
-  unsigned col_next[2];    // column-emission work counter of each window slot
+  unsigned long long full[KW_NCH], empty[KW_NCH], bm_full[KW_NWS], win_done[KW_NWS];
+  unsigned col_next[KW_NWS];  // column-emission work counter of each window slot
   WinItem items[4];        // producer's work-item ring (loaded two windows ahead)
   int pscan[2][KW_PW + 1];
   int pexcl[KW_NP + 1];
   int64_t ticket;
 };
+static_assert(sizeof(KwShared) <= 227 * 1024, "k_win shared memory");
+
 
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
@@ -1986,8 +1995,8 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   bool copy_pending = false;
   const WinItem* copy_item = nullptr;
   unsigned copy_slot = 0, copy_wseq = 0;
-  int64_t prev_base[2] = {0, 0};  // C offset / values of the window last loaded into each slot
-  int prev_cnt[2] = {0, 0};
+  int64_t prev_base[KW_NWS];  // C offset / values of the window last loaded into each slot
+  int prev_cnt[KW_NWS];
   // wait until the consumers are done with the window in slot ws (its u-th
   // use), then store its values
   auto release = [&](unsigned ws, unsigned u) {
@@ -1998,7 +2007,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   auto publish = [&](int flags, const WinItem& it, unsigned wslot) {
     if (copy_pending) {
       KW_T0();
-      if (copy_wseq >= 2) release(copy_slot, (copy_wseq >> 1) - 1u);
+      if (copy_wseq >= KW_NWS) release(copy_slot, copy_wseq / KW_NWS - 1u);
       KW_ACC(pc_free);
       prev_base[copy_slot] = copy_item->out_base;
       prev_cnt[copy_slot] = copy_item->cnt;
@@ -2195,7 +2204,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
       load_item(kcur + 3);
       copy_pending = true;
       copy_item = &sh.items[kcur & 3];
-      copy_slot = wseq & 1u;
+      copy_slot = wseq % KW_NWS;
       copy_wseq = wseq;
       acquire();
       flags = KW_FIRST;
@@ -2210,7 +2219,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
       KW_ACC(pc_clip);
     }
     const WinItem it = sh.items[c0.k & 3];
-    const unsigned wslot = wseq & 1u;
+    const unsigned wslot = wseq % KW_NWS;
     append(bs0, len0, a0, flags, it, wslot);  // stage 2
     if (c1.k != c0.k) {  // c0 was the window's last batch
       publish(flags | KW_LAST, it, wslot);
@@ -2228,7 +2237,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   WinItem none{};
   publish(KW_END, none, 0);
   // the last window of each slot
-  for (unsigned w = wseq >= 2 ? wseq - 2 : 0; w < wseq; ++w) release(w & 1u, w >> 1);
+  for (unsigned w = wseq >= KW_NWS ? wseq - KW_NWS : 0; w < wseq; ++w) release(w % KW_NWS, w / KW_NWS);
   if (sizeof(V) == 8 && tid == 0) bulk_wait_all();  // value stores complete before exit
 #ifdef SG_PROF
   if (tid == 0) {
@@ -2250,7 +2259,9 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
   const int32_t* __restrict__ b_col = B.col;
   const V* __restrict__ b_val = (const V*)B.val;
   unsigned cseq = 0;
-  unsigned wuse[2] = {0u, 0u};
+  unsigned wuse[KW_NWS];
+#pragma unroll
+  for (int j = 0; j < KW_NWS; ++j) wuse[j] = 0u;
   unsigned long long cc_full = 0, cc_bm = 0, cc_grp = 0, cc_col = 0, cc_store = 0;
   (void)cc_full; (void)cc_bm; (void)cc_grp; (void)cc_col; (void)cc_store;
   for (;;) {
@@ -2480,13 +2491,13 @@ __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* 
                                                   int kw_skip) {
   extern __shared__ __align__(128) unsigned char kw_smem[];
   KwShared& sh = *reinterpret_cast<KwShared*>(kw_smem);
-  for (int i = threadIdx.x; i < 2 * KW_VSLOT; i += KW_NT) (&sh.vals[0][0])[i] = 0.0;
+  for (int i = threadIdx.x; i < KW_NWS * KW_VSLOT; i += KW_NT) (&sh.vals[0][0])[i] = 0.0;
   if (threadIdx.x == 0) {
     for (int j = 0; j < KW_NCH; ++j) {
       mbar_init(&sh.full[j], KW_NP);
       mbar_init(&sh.empty[j], KW_CW);
     }
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < KW_NWS; ++j) {
       mbar_init(&sh.bm_full[j], 1);
       mbar_init(&sh.win_done[j], KW_CW * 32);
       sh.col_next[j] = 0;

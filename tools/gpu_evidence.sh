@@ -18,4 +18,3 @@ done
 timeout 1200 ncu --set full --clock-control none --import-source on -k k_win -c 1 -o gpurun_out/ev_full_k_win -f python tools/run_once.py rmat20 > /dev/null 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_bitmap -c 1 -o gpurun_out/ev_full_count -f python tools/run_once.py rmat20 > /dev/null 2>&1
 ls -la gpurun_out/ev_*
-bash tools/sanitize.sh
