@@ -2838,6 +2838,9 @@ __device__ __forceinline__ int64_t pow2_at_least(int64_t x) {
 // products / crc, crc the conservative sampled CR (predict.py:111-118),
 // instead of by products; a row whose table fills is flagged (-1) by the count
 // kernel and recounted with product sizing (rerun = 1 classifies only those).
+#ifndef SG_BM_COUNT_MIN
+#define SG_BM_COUNT_MIN 4096
+#endif
 __global__ void k_classify_count(int64_t m, const int64_t* __restrict__ products, const int64_t* __restrict__ lo,
                                  const int64_t* __restrict__ hi, uint8_t* __restrict__ bins,
                                  int64_t* __restrict__ counts, double crc, int rerun, int64_t skip_max) {
@@ -2857,7 +2860,9 @@ __global__ void k_classify_count(int64_t m, const int64_t* __restrict__ products
     const int64_t span = hi[i] - lo[i] + 1;
     const int64_t est = (crc > 1.0 && !rerun) ? max((int64_t)1, (int64_t)ceil((double)p / crc)) : p;
     const int64_t T = max(pow2_at_least(2 * est), (int64_t)32);
-    if (count_uses_bitmap(p, span)) {
+    // rows of more than SG_BM_COUNT_MIN products are counted with a bitmap
+    // even when it is sparse (no windows for them: k_win_capacity)
+    if (count_uses_bitmap(p, span) || (SG_BM_COUNT_MIN > 0 && p > SG_BM_COUNT_MIN && span <= ((int64_t)1 << 20))) {
       b = bm_bin(span);
     } else if (est <= 1024) {
       b = (uint8_t)(BIN_HW0 + log2_pow2(T) - 5);
