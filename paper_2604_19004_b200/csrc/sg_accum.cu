@@ -1939,6 +1939,17 @@ __device__ __forceinline__ void kw_clip(const KwEnt& en, const int32_t* __restri
   len = (int)(ee - ss);
 }
 
+// fp64 window values leave through the copy engine (SG_KW_BULK=0: plain
+// stores by the producer threads -- e.g. for compute-sanitizer initcheck,
+// which does not see the copy engine's global writes)
+#ifndef SG_KW_BULK
+#define SG_KW_BULK 1
+#endif
+template <typename V>
+__host__ __device__ constexpr bool kw_bulk() {
+  return sizeof(V) == 8 && SG_KW_BULK;
+}
+
 // Store the values of the window that held slot ws (all consumer warps have
 // arrived on win_done[ws]) and leave the slot zeroed (float) or to be zeroed
 // by the next bulk load (fp64).  fp64: tid 0 hands them to the copy engine --
@@ -1949,7 +1960,7 @@ __device__ __forceinline__ void kw_store_window(KwShared& sh, unsigned ws, V* __
                                                 int64_t out_base, int cnt, int tid) {
   const uint32_t vs = smem_u32(&sh.vals[ws][0]);
   V* dst = out_val + out_base;
-  if constexpr (sizeof(V) == 8) {
+  if constexpr (kw_bulk<V>()) {
     if (tid == 0) {
       const uint32_t vshift = (uint32_t)((reinterpret_cast<uintptr_t>(dst) >> 3) & 1u);  // see KW_VSLOT
       const int head = (int)vshift < cnt ? (int)vshift : 0;
@@ -2002,7 +2013,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   auto release = [&](unsigned ws, unsigned u) {
     mbar_wait(&sh.win_done[ws], u & 1u);
     kw_store_window<V>(sh, ws, out_val, prev_base[ws], prev_cnt[ws], tid);
-    if (sizeof(V) != 8) pbar();
+    if (!kw_bulk<V>()) pbar();
   };
   auto publish = [&](int flags, const WinItem& it, unsigned wslot) {
     if (copy_pending) {
@@ -2015,7 +2026,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
         sh.col_next[copy_slot] = 0;
         const unsigned nwords = (unsigned)(((int64_t)copy_item->c1 - copy_item->c0 + 63) >> 6);
         // fp64: the slot's values [0, shift + cnt) re-zeroed by the copy engine
-        const unsigned zb = sizeof(V) == 8 ? ((1u + (unsigned)copy_item->cnt) * 8u + 15u) & ~15u : 0u;
+        const unsigned zb = kw_bulk<V>() ? ((1u + (unsigned)copy_item->cnt) * 8u + 15u) & ~15u : 0u;
         mbar_arrive_tx(&sh.bm_full[copy_slot], nwords * 16u + zb);
         bulk_g2s(&sh.bm[copy_slot][0], bm16 + copy_item->bm_word, nwords * 16u, &sh.bm_full[copy_slot]);
         if (zb) bulk_g2s(&sh.vals[copy_slot][0], g_kw_zero, zb, &sh.bm_full[copy_slot]);
@@ -2238,7 +2249,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
   publish(KW_END, none, 0);
   // the last window of each slot
   for (unsigned w = wseq >= KW_NWS ? wseq - KW_NWS : 0; w < wseq; ++w) release(w % KW_NWS, w / KW_NWS);
-  if (sizeof(V) == 8 && tid == 0) bulk_wait_all();  // value stores complete before exit
+  if (kw_bulk<V>() && tid == 0) bulk_wait_all();  // value stores complete before exit
 #ifdef SG_PROF
   if (tid == 0) {
     atomicAdd(&g_kw[0], pc_free);
@@ -2287,7 +2298,8 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
     const long long _kg = clock64();
 #endif
     // (see KW_VSLOT) values from slot element 1 when C's first value is not 16-byte aligned
-    const uint32_t vshift = sizeof(V) == 8 ? (uint32_t)((reinterpret_cast<uintptr_t>(out_val + out_base) >> 3) & 1u) : 0u;
+    const uint32_t vshift =
+        kw_bulk<V>() ? (uint32_t)((reinterpret_cast<uintptr_t>(out_val + out_base) >> 3) & 1u) : 0u;
     WinAddOp op{smem_u32(&sh.bm[ws][0]), smem_u32(&sh.vals[ws][0]) + (vshift - (uint32_t)rank0) * 8u, c0};
     const uint32_t grp_s = smem_u32(&ch.grp[0]), d_s = smem_u32(&ch.d[0]), av_s = smem_u32(&ch.av[0]);
     for (;;) {
