@@ -583,6 +583,8 @@ def main():
         roof["traffic"] = ncu_traffic(args.config, dk)
         roof["dominant_kernel"] = dk
         roof["traffic_source"] = "profiles/ncu_traffic.json (dominant kernel, per launch)"
+    # the whole multiply against the same HBM roof (algorithmic bytes / step time)
+    roof["whole_step"] = {"achieved": step_gbs, "frac": step_gbs / peak, "algorithmic_bytes_per_step": alg}
     roof["kernel_ms_per_step"] = {kk: round(v[0] / args.steps, 3) for kk, v in ktimes.items()}
     roof["kernel_ms_note"] = ("CUDA-event brackets on the launching stream; bin kernels (k_hash_*, k_bitmap) "
                               "run concurrently on side streams, so their brackets overlap")
