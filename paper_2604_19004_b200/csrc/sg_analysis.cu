@@ -65,6 +65,74 @@ static void ktimer_clear() {
 // ---------------------------------------------------------------------------
 // row statistics: G lanes per A row
 
+// A rows longer than RS_LONG entries (R-MAT hub rows: tens of thousands)
+// take a whole block each instead of G lanes: blocks sweep the rows 256 at a
+// time, collect the long ones and reduce each with all their threads.
+constexpr int64_t RS_LONG = 512;
+constexpr int RS_NT = 256;
+
+__global__ void __launch_bounds__(RS_NT) k_row_stats_long(int64_t m, int64_t b_ncols,
+                                                          const int64_t* __restrict__ a_ptr,
+                                                          const int32_t* __restrict__ a_col,
+                                                          const int64_t* __restrict__ b_ptr,
+                                                          const int32_t* __restrict__ b_col,
+                                                          int64_t* __restrict__ products,
+                                                          int64_t* __restrict__ span_lo,
+                                                          int64_t* __restrict__ span_hi,
+                                                          unsigned long long* __restrict__ totals) {
+  __shared__ int64_t list[RS_NT];
+  __shared__ int nlist;
+  __shared__ int64_t red[3][RS_NT / 32];
+  const int w = threadIdx.x >> 5, lane = lane_id();
+  for (int64_t base = (int64_t)blockIdx.x * RS_NT; base < m; base += (int64_t)gridDim.x * RS_NT) {
+    if (threadIdx.x == 0) nlist = 0;
+    __syncthreads();
+    const int64_t r = base + threadIdx.x;
+    if (r < m && a_ptr[r + 1] - a_ptr[r] > RS_LONG) list[atomicAdd(&nlist, 1)] = r;
+    __syncthreads();
+    const int n = nlist;
+    __syncthreads();  // (nlist is reset by the next sweep step)
+    for (int i = 0; i < n; ++i) {
+      const int64_t row = list[i];
+      int64_t prod = 0, lo = b_ncols, hi = -1;
+      const int64_t e = a_ptr[row + 1];
+      for (int64_t t = a_ptr[row] + threadIdx.x; t < e; t += RS_NT) {
+        const int32_t k = a_col[t];
+        const int64_t bs = b_ptr[k], be = b_ptr[k + 1];
+        if (be > bs) {
+          prod += be - bs;
+          lo = min(lo, (int64_t)b_col[bs]);
+          hi = max(hi, (int64_t)b_col[be - 1]);
+        }
+      }
+      prod = warp_sum(prod);
+      lo = warp_min(lo);
+      hi = warp_max(hi);
+      if (lane == 0) {
+        red[0][w] = prod;
+        red[1][w] = lo;
+        red[2][w] = hi;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int j = 1; j < RS_NT / 32; ++j) {
+          prod += red[0][j];
+          lo = min(lo, red[1][j]);
+          hi = max(hi, red[2][j]);
+        }
+        products[row] = prod;
+        span_lo[row] = prod ? lo : b_ncols;
+        span_hi[row] = prod ? hi : -1;
+        if (prod) {
+          atomicAdd(&totals[0], (unsigned long long)prod);
+          atomicMax(&totals[1], (unsigned long long)prod);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <int G>
 __global__ void __launch_bounds__(256) k_row_stats(int64_t m, int64_t b_ncols,
                                                    const int64_t* __restrict__ a_ptr,
@@ -79,7 +147,12 @@ __global__ void __launch_bounds__(256) k_row_stats(int64_t m, int64_t b_ncols,
   const int64_t row = gid / G;
   const int sub = (int)(gid % G);
   int64_t prod = 0, lo = b_ncols, hi = -1;
-  if (row < m) {
+  bool mine_row = row < m;
+  if (mine_row) {
+    const int64_t e = a_ptr[row + 1];
+    mine_row = e - a_ptr[row] <= RS_LONG;  // long rows: k_row_stats_long
+  }
+  if (mine_row) {
     const int64_t e = a_ptr[row + 1];
     for (int64_t t = a_ptr[row] + sub; t < e; t += G) {
       const int32_t k = a_col[t];
@@ -97,13 +170,13 @@ __global__ void __launch_bounds__(256) k_row_stats(int64_t m, int64_t b_ncols,
     lo = min(lo, (int64_t)__shfl_xor_sync(SG_FULL, lo, o, G));
     hi = max(hi, (int64_t)__shfl_xor_sync(SG_FULL, hi, o, G));
   }
-  if (row < m && sub == 0) {
+  if (mine_row && sub == 0) {
     products[row] = prod;
     span_lo[row] = prod ? lo : b_ncols;
     span_hi[row] = prod ? hi : -1;
   }
   // block partials -> one atomic per warp
-  int64_t mine = (row < m && sub == 0) ? prod : 0;
+  int64_t mine = (mine_row && sub == 0) ? prod : 0;
   int64_t s = warp_sum(mine);
   int64_t mx = warp_max(mine);
   if (lane_id() == 0) {
@@ -578,7 +651,10 @@ int sg_row_stats(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t
   constexpr int G = 8;
   k_row_stats<G><<<grid_for(m * G, 256), 256, 0, s>>>(m, b_ncols, a_ptr, a_col, b_ptr, b_col, products,
                                                       span_lo, span_hi, (unsigned long long*)totals2);
-  return check_cuda("sg_row_stats");
+  const int gl = (int)std::min<int64_t>((m + RS_NT - 1) / RS_NT, 148 * 8);  // 8 sweeping blocks per SM
+  k_row_stats_long<<<gl, RS_NT, 0, s>>>(m, b_ncols, a_ptr, a_col, b_ptr, b_col, products, span_lo, span_hi,
+                                         (unsigned long long*)totals2);
+  return check_cuda("sg_row_stats", 2);
 }
 
 int sg_hll_build(int64_t k, const int64_t* b_ptr, const int32_t* b_col, int p, uint8_t* regs,
