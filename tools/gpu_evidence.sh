@@ -18,3 +18,5 @@ done
 timeout 1200 ncu --set full --clock-control none --import-source on -k k_win -c 1 -o gpurun_out/ev_full_k_win -f python tools/run_once.py rmat20 > /dev/null 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_bitmap -c 1 -o gpurun_out/ev_full_count -f python tools/run_once.py rmat20 > /dev/null 2>&1
 ls -la gpurun_out/ev_*
+SAN_TIMEOUT=900 bash tools/sanitize.sh memcheck synccheck
+SANITIZE_ONLY=stress timeout 1200 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 50 python tools/sanitize_cases.py > gpurun_out/sanitize_racecheck_stress.txt 2>&1; echo "racecheck(stress) rc=$? $(grep -E 'RACECHECK SUMMARY|sanitize cases ok' gpurun_out/sanitize_racecheck_stress.txt | tr '\n' ' ')"
