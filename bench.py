@@ -337,7 +337,7 @@ def check_parity(a, b, rows, cb):
             "row_blocks": [list(x) for x in rows]}
 
 
-TIMED_KERNELS = ("k_win", "k_bmr", "k_win_light", "k_expand", "k_hash_warp", "k_hash_block", "k_bitmap",
+TIMED_KERNELS = ("k_win", "k_bmr", "k_win_light", "k_hash_warp", "k_hash_block", "k_bitmap",
                  "k_hash_warp:count", "k_hash_block:count", "k_bitmap:count")
 
 

@@ -2264,7 +2264,7 @@ __device__ __forceinline__ void kw_producer(KwShared& sh, int64_t nwork, const W
 
 template <typename V>
 __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t* __restrict__ out_col,
-                                            V* __restrict__ out_val, int kw_skip) {
+                                            V* __restrict__ out_val) {
   const int lane = lane_id();
   const unsigned le = lanemask_le();
   const int32_t* __restrict__ b_col = B.col;
@@ -2307,7 +2307,6 @@ __device__ __forceinline__ void kw_consumer(KwShared& sh, const Csr& B, int32_t*
       if (lane == 0) g0 = atomicAdd(&ch.next, (unsigned)KW_U);
       g0 = __shfl_sync(SG_FULL, g0, 0);
       if ((int)g0 >= ng) break;
-      if (kw_skip) continue;  // timing experiment: producer-bound time (SG_KW_SKIP=1)
       int32_t col[KW_U];
       double v[KW_U];
       if (((int)g0 + KW_U) * 32 <= P) {
@@ -2499,8 +2498,7 @@ template <typename V>
 __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* __restrict__ work, Csr A, Csr B,
                                                   BTile bt, const uint4* __restrict__ bm16,
                                                   const KwEnt* __restrict__ hent, int32_t* __restrict__ out_col,
-                                                  V* __restrict__ out_val, unsigned long long* __restrict__ ticket,
-                                                  int kw_skip) {
+                                                  V* __restrict__ out_val, unsigned long long* __restrict__ ticket) {
   extern __shared__ __align__(128) unsigned char kw_smem[];
   KwShared& sh = *reinterpret_cast<KwShared*>(kw_smem);
   for (int i = threadIdx.x; i < KW_NWS * KW_VSLOT; i += KW_NT) (&sh.vals[0][0])[i] = 0.0;
@@ -2520,169 +2518,9 @@ __global__ void __launch_bounds__(KW_NT, 1) k_win(int64_t nwork, const WinItem* 
   if (warp_id() < KW_PW)
     kw_producer<V>(sh, nwork, work, A, B, bt, bm16, hent, out_val, ticket);
   else
-    kw_consumer<V>(sh, B, out_col, out_val, kw_skip);
+    kw_consumer<V>(sh, B, out_col, out_val);
 }
 
-// Column expansion of the long rows from the saved key bitmaps:
-// C.col_idx[row_ptr[row] + rank ..] for every set bit, ascending.  Blocks
-// sweep the window work items (each <= WIN_WORDS words, so the work is even).
-// Each block step loads U * NT bitmap words (coalesced, word (u, t) at
-// u * NT + t) and ranks them itself -- per-warp shuffle scans of the
-// popcounts, the U x NT/32 warp totals scanned again by every warp (no extra
-// barrier), a running carry across steps -- so it reads 8 B per word instead
-// of 12 with the saved word ranks.  The step's columns are staged in shared
-// memory and leave as aligned 16-byte stores.  R-MAT-20: 58 -> 35 ms (direct
-// per-lane stores with saved ranks 58, self-ranked direct 45, staged
-// CAP 4096 37, CAP 6144 35; CAP-sized multi-pass staging of dense steps 48).
-constexpr int EXP_NT = 256;
-
-template <int NT, int U, int CAP>
-__global__ void __launch_bounds__(NT, 2048 / NT) k_expand_scan(int64_t nwork, const WinItem* __restrict__ work,
-                                                    const unsigned long long* __restrict__ bm_save,
-                                                    int32_t* __restrict__ out_col) {
-  static_assert(U * (NT / 32) == 32, "one warp scans the warp totals");
-  __shared__ int wtot[2][32];
-  static_assert(CAP % 4 == 0, "16-byte staging passes");
-  __shared__ __align__(16) int sbuf[CAP];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int par = 0;
-  for (int64_t b = blockIdx.x; b < nwork; b += gridDim.x) {
-    const WinItem it = work[b];
-    if (it.bm_word < 0) continue;
-    const int64_t nw = ((int64_t)it.c1 - it.c0 + 63) >> 6;
-    const uint4* bm = reinterpret_cast<const uint4*>(bm_save) + it.bm_word;
-    int32_t* out = out_col + it.out_base;
-    int carry = 0;
-    for (int64_t i0 = 0; i0 < nw; i0 += U * NT) {
-      unsigned long long bits[U];
-      int pre[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * NT + threadIdx.x;
-        if (i < nw) {
-          const uint4 q = __ldcs(bm + i);
-          bits[u] = ((unsigned long long)q.z << 32) | q.x;
-        } else {
-          bits[u] = 0ull;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = __popcll(bits[u]);
-        int x = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, x, d);
-          if (lane >= d) x += y;
-        }
-        pre[u] = x - c;
-        if (lane == 31) wtot[par][u * (NT / 32) + warp] = x;
-      }
-      __syncthreads();
-      const int t = wtot[par][lane];
-      int x = t;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, d);
-        if (lane >= d) x += y;
-      }
-      const int total = __shfl_sync(0xffffffffu, x, 31);
-      // the staging buffer is shifted by the output's misalignment so the
-      // copy-out moves aligned 16-byte vectors; a step with more than CAP
-      // entries (dense hub-row words) writes straight to global memory
-      const int mis = (int)(((uintptr_t)(out + carry) & 15) >> 2);
-      const int end = mis + total;
-      const bool staged = end <= CAP;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int base = __shfl_sync(0xffffffffu, x - t, u * (NT / 32) + warp) + pre[u];
-        const int32_t cb = it.c0 + (int32_t)(64 * (i0 + u * NT + threadIdx.x));
-        emit_bits(bits[u], cb, staged ? sbuf + mis + base : out + carry + base);
-      }
-      if (staged) {
-        __syncthreads();
-        int32_t* oa = out + carry - mis;
-        for (int q = threadIdx.x; q < (end + 3) >> 2; q += NT) {
-          const int4 v = reinterpret_cast<const int4*>(sbuf)[q];
-          const int e0 = 4 * q;
-          if (e0 >= mis && e0 + 4 <= end) {
-            reinterpret_cast<int4*>(oa)[q] = v;
-          } else {
-            if (e0 >= mis) oa[e0] = v.x;
-            if (e0 + 1 >= mis && e0 + 1 < end) oa[e0 + 1] = v.y;
-            if (e0 + 2 >= mis && e0 + 2 < end) oa[e0 + 2] = v.z;
-            if (e0 + 3 >= mis && e0 + 3 < end) oa[e0 + 3] = v.w;
-          }
-        }
-      }
-      carry += total;
-      par ^= 1;
-    }
-  }
-}
-
-// Column expansion from the saved 16-byte words, whose stored row ranks give
-// every word's output position directly: no scan and no rank barrier; the
-// step's columns are staged in shared memory (double-buffered, shifted by the
-// output's misalignment) and leave as aligned 16-byte stores, so a step costs
-// one block barrier.
-template <int NT, int U, int CAP>
-__global__ void __launch_bounds__(NT) k_expand_rank(int64_t nwork, const WinItem* __restrict__ work,
-                                                    const uint4* __restrict__ bm16, int32_t* __restrict__ out_col) {
-  static_assert(CAP % 4 == 0, "16-byte staging passes");
-  __shared__ __align__(16) int sbuf[2][CAP];
-  int par = 0;
-  for (int64_t b = blockIdx.x; b < nwork; b += gridDim.x) {
-    const WinItem it = work[b];
-    if (it.bm_word < 0) continue;
-    const int64_t nw = ((int64_t)it.c1 - it.c0 + 63) >> 6;
-    const uint4* bm = bm16 + it.bm_word;
-    int32_t* out = out_col + it.out_base;
-    const uint32_t r0 = (uint32_t)it.rank0;
-    for (int64_t i0 = 0; i0 < nw; i0 += U * NT) {
-      uint4 q[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * NT + threadIdx.x;
-        q[u] = i < nw ? __ldcs(bm + i) : make_uint4(0u, 0u, 0u, 0u);
-      }
-      const uint32_t sb = (i0 == 0 ? r0 : __ldg(&bm[i0].y)) - r0;  // step base (window-relative)
-      const uint32_t se = (i0 + U * NT < nw ? __ldg(&bm[i0 + U * NT].y) - r0 : (uint32_t)it.cnt);
-      const int total = (int)(se - sb);
-      int32_t* o = out + sb;
-      const int mis = (int)(((uintptr_t)o & 15) >> 2);
-      const int end = mis + total;
-      const bool staged = end <= CAP;
-      int* buf = sbuf[par];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t i = i0 + u * NT + threadIdx.x;
-        if (i < nw && (q[u].x | q[u].z)) {
-          const int32_t cb = it.c0 + (int32_t)(64 * i);
-          const int p0 = (int)(q[u].y - r0 - sb);
-          emit_bits(((unsigned long long)q[u].z << 32) | q[u].x, cb, staged ? buf + mis + p0 : o + p0);
-        }
-      }
-      if (staged) {
-        __syncthreads();
-        int32_t* oa = o - mis;
-        for (int k = threadIdx.x; k < (end + 3) >> 2; k += NT) {
-          const int4 v = reinterpret_cast<const int4*>(buf)[k];
-          const int e0 = 4 * k;
-          if (e0 >= mis && e0 + 4 <= end) {
-            reinterpret_cast<int4*>(oa)[k] = v;
-          } else {
-            if (e0 >= mis) oa[e0] = v.x;
-            if (e0 + 1 >= mis && e0 + 1 < end) oa[e0 + 1] = v.y;
-            if (e0 + 2 >= mis && e0 + 2 < end) oa[e0 + 2] = v.z;
-            if (e0 + 3 >= mis && e0 + 3 < end) oa[e0 + 3] = v.w;
-          }
-        }
-        par ^= 1;  // the next step stages into the other buffer
-      }
-    }
-  }
-}
 
 // Work items: one per used window, grouped into NBUCKET column-range buckets
 // (bucket = c0 * NBUCKET / ncols) so the dynamic ticket order sweeps B's
@@ -3187,16 +3025,6 @@ static int light_len() {
 }
 
 
-// C's columns of the windowed rows written by k_win itself (1, default) or by
-// the separate expansion kernel (SG_FUSE_COLS=0)
-static bool fuse_cols() {
-  static bool v = [] {
-    const char* e = getenv("SG_FUSE_COLS");
-    return e ? atoi(e) != 0 : true;
-  }();
-  return v;
-}
-
 // window scratch: WinItems, then the heavy and light entry tables (indexed by
 // A position) and their per-row counts
 struct WinScratch {
@@ -3233,12 +3061,8 @@ static int launch_kwin(int64_t n, const WinItem* work, const Csr& A, const Csr& 
   auto kern = k_win<V>;
   if (int rc = set_smem(kern, sm)) return rc;
   const int grid = (int)std::min<int64_t>(n, (int64_t)num_sms());
-  static const int skip = [] {
-    const char* e = getenv("SG_KW_SKIP");
-    return e ? atoi(e) : 0;
-  }();
   kern<<<grid, KW_NT, sm, s>>>(n, work, A, B, bt, reinterpret_cast<const uint4*>(W.bm_save), hent, out_col,
-                               (V*)out_val, ticket, skip);
+                               (V*)out_val, ticket);
   return check_cuda("k_win");
 }
 
@@ -3447,13 +3271,6 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
                                                  out_off, W.bm_save ? W.bm_off : nullptr,
                                                  W.bm_save ? wsc.hcnt : nullptr, cnt, work);
   if (int rc = check_cuda("k_win_scatter")) return rc;
-  if (W.bm_save && !fuse_cols()) {
-    ktimer_begin("k_expand", s);
-    k_expand_rank<EXP_NT, 4, 6144><<<(int)std::min<int64_t>(nwork, (int64_t)num_sms() * 4), EXP_NT, 0, s>>>(
-        nwork, work, reinterpret_cast<const uint4*>(W.bm_save), out_col);
-    ktimer_end(s);
-    if (int rc = check_cuda("k_expand")) return rc;
-  }
   if (const char* dump = getenv("SG_DUMP_WINDOWS")) {
     // analysis hook: the window work items as raw 48-byte records
     std::vector<WinItem> hw((size_t)nwork);
@@ -3471,9 +3288,8 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   if (W.bm_save) {
     // saved bitmaps: the warp-specialised window kernel takes every window
     // (both size classes, in ticket order), heavy entries only
-    int32_t* kcol = fuse_cols() ? out_col : nullptr;
-    int rc = dtype == SG_F64 ? launch_kwin<double>(nwork, work, A, B, bt, W, wsc.hent, kcol, out_val, tickets, s)
-                             : launch_kwin<float>(nwork, work, A, B, bt, W, wsc.hent, kcol, out_val, tickets, s);
+    int rc = dtype == SG_F64 ? launch_kwin<double>(nwork, work, A, B, bt, W, wsc.hent, out_col, out_val, tickets, s)
+                             : launch_kwin<float>(nwork, work, A, B, bt, W, wsc.hent, out_col, out_val, tickets, s);
     if (rc) return rc;
     ktimer_end(s);
     // then the light entries add on top of the stored window values
