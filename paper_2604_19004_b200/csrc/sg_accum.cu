@@ -1154,6 +1154,19 @@ struct Win {
 // Symbolic-pass routing: rows counted with a shared-memory bitmap (and hence
 // able to record numeric windows).  Long rows with a dense enough span, and
 // every row too long for the largest count hash table.
+// rows of more than SG_BM_COUNT_MIN products are counted with a bitmap even
+// when it is sparse (span/64 > products); with SG_SPARSE_WIN they also get
+// windows (cut by the count pass, no saved words) taken by k_bmr
+#ifndef SG_BM_COUNT_MIN
+#define SG_BM_COUNT_MIN 4096
+#endif
+#ifndef SG_SPARSE_WIN
+#define SG_SPARSE_WIN 0
+#endif
+__host__ __device__ __forceinline__ bool count_uses_bitmap(int64_t p, int64_t span);
+__host__ __device__ __forceinline__ bool count_bitmap_sparse(int64_t p, int64_t span) {
+  return !count_uses_bitmap(p, span) && SG_BM_COUNT_MIN > 0 && p > SG_BM_COUNT_MIN && span <= ((int64_t)1 << 20);
+}
 __host__ __device__ __forceinline__ bool count_uses_bitmap(int64_t p, int64_t span) {
   if (p <= 1024) return false;
   if (span <= ((int64_t)1 << 20) && (span + 63) / 64 <= p) return true;
@@ -1309,9 +1322,10 @@ __global__ void __launch_bounds__(NT) k_bitmap(int64_t nbin, const int32_t* __re
       // pass (pre[t] = rank of tile t); MODE 1: word ranks for the values
       const int64_t wtot =
           MODE == 0 ? prefix_save<NT>(bm, nwords, total,
-                                      win.bm_save ? reinterpret_cast<uint4*>(win.bm_save) + win.bm_off[row] +
-                                                        ((wlo - org) >> 6)
-                                                  : nullptr,
+                                      (win.bm_save && win.bm_off[row + 1] > win.bm_off[row])
+                                          ? reinterpret_cast<uint4*>(win.bm_save) + win.bm_off[row] +
+                                                ((wlo - org) >> 6)
+                                          : nullptr,
                                       pre, scr)
                     : bitmap_prefix<NT>(bm, pre, nwords, scr);
       if (MODE == 0) {
@@ -2552,17 +2566,21 @@ __device__ __forceinline__ void for_each_window(const int2* wr, int n, int64_t r
   }
 }
 
+// window class: 2 = the row's words were saved (k_win), else the k_bmr
+// geometry class (win_class)
 __global__ void k_win_counts(int64_t m, int64_t ncols, const int64_t* __restrict__ win_off,
                              const int2* __restrict__ wins, const int32_t* __restrict__ nwin,
                              const int64_t* __restrict__ span_hi, const int64_t* __restrict__ out_off,
-                             unsigned long long* __restrict__ bucket_cnt) {
+                             const int64_t* __restrict__ bm_off, unsigned long long* __restrict__ bucket_cnt) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const int n = nwin[i];
   if (n <= 0) return;
+  const bool saved = bm_off && bm_off[i + 1] > bm_off[i];
   for_each_window(wins + win_off[i], n, out_off[i + 1] - out_off[i], (int32_t)(span_hi[i] + 1),
                   [&](int32_t c0, int32_t c1, bool, int64_t cnt, int32_t) {
-                    atomicAdd(&bucket_cnt[win_class(cnt, c0, c1) * NBUCKET + win_bucket(c0, ncols)], 1ull);
+                    const int cls = saved ? 2 : win_class(cnt, c0, c1);
+                    atomicAdd(&bucket_cnt[cls * NBUCKET + win_bucket(c0, ncols)], 1ull);
                   });
 }
 
@@ -2577,6 +2595,7 @@ __global__ void k_win_scatter(int64_t m, int64_t ncols, const int64_t* __restric
   const int n = nwin[i];
   if (n <= 0) return;
   const int64_t org = win_origin(span_lo[i]);
+  const bool saved = bm_off && bm_off[i + 1] > bm_off[i];
   for_each_window(wins + win_off[i], n, out_off[i + 1] - out_off[i], (int32_t)(span_hi[i] + 1),
                   [&](int32_t c0, int32_t c1, bool last, int64_t cnt, int32_t rank0) {
                     WinItem it;
@@ -2587,11 +2606,11 @@ __global__ void k_win_scatter(int64_t m, int64_t ncols, const int64_t* __restric
                     it.out_base = out_off[i] + rank0;
                     it.t0 = a_ptr[i];
                     // k_win walks the row's heavy entry table (same A offset)
-                    it.t_len = heavy_cnt ? heavy_cnt[i] : (int32_t)(a_ptr[i + 1] - a_ptr[i]);
-                    it.bm_word = bm_off ? bm_off[i] + ((int64_t)c0 - org) / 64 : -1;
+                    it.t_len = (saved && heavy_cnt) ? heavy_cnt[i] : (int32_t)(a_ptr[i + 1] - a_ptr[i]);
+                    it.bm_word = saved ? bm_off[i] + ((int64_t)c0 - org) / 64 : -1;
                     it.rank0 = rank0;
-                    const unsigned long long slot =
-                        atomicAdd(&cursor[win_class(cnt, c0, c1) * NBUCKET + win_bucket(c0, ncols)], 1ull);
+                    const int cls = saved ? 2 : win_class(cnt, c0, c1);
+                    const unsigned long long slot = atomicAdd(&cursor[cls * NBUCKET + win_bucket(c0, ncols)], 1ull);
                     work[slot] = it;
                   });
 }
@@ -2651,7 +2670,8 @@ __global__ void k_win_capacity(int64_t m, const int64_t* __restrict__ products, 
   // symbolic pass: only rows the count classifier sends to a bitmap kernel;
   // fallback count pass (select given): every selected long row
   const bool sel = select == nullptr ? count_uses_bitmap(p, span) : (select[i] && p > 256);
-  cap[i] = sel ? window_capacity(p, span) : 0;
+  const bool thin = SG_SPARSE_WIN && select == nullptr && count_bitmap_sparse(p, span);  // windows, no words
+  cap[i] = (sel || thin) ? window_capacity(p, span) : 0;
   if (words) words[i] = sel ? (hi[i] - win_origin(lo[i])) / 64 + 1 : 0;
 }
 
@@ -2688,9 +2708,6 @@ __device__ __forceinline__ int64_t pow2_at_least(int64_t x) {
 // products / crc, crc the conservative sampled CR (predict.py:111-118),
 // instead of by products; a row whose table fills is flagged (-1) by the count
 // kernel and recounted with product sizing (rerun = 1 classifies only those).
-#ifndef SG_BM_COUNT_MIN
-#define SG_BM_COUNT_MIN 4096
-#endif
 __global__ void k_classify_count(int64_t m, const int64_t* __restrict__ products, const int64_t* __restrict__ lo,
                                  const int64_t* __restrict__ hi, uint8_t* __restrict__ bins,
                                  int64_t* __restrict__ counts, double crc, int rerun, int64_t skip_max) {
@@ -2710,9 +2727,7 @@ __global__ void k_classify_count(int64_t m, const int64_t* __restrict__ products
     const int64_t span = hi[i] - lo[i] + 1;
     const int64_t est = (crc > 1.0 && !rerun) ? max((int64_t)1, (int64_t)ceil((double)p / crc)) : p;
     const int64_t T = max(pow2_at_least(2 * est), (int64_t)32);
-    // rows of more than SG_BM_COUNT_MIN products are counted with a bitmap
-    // even when it is sparse (no windows for them: k_win_capacity)
-    if (count_uses_bitmap(p, span) || (SG_BM_COUNT_MIN > 0 && p > SG_BM_COUNT_MIN && span <= ((int64_t)1 << 20))) {
+    if (count_uses_bitmap(p, span) || count_bitmap_sparse(p, span)) {
       b = bm_bin(span);
     } else if (est <= 1024) {
       b = (uint8_t)(BIN_HW0 + log2_pow2(T) - 5);
@@ -3228,23 +3243,26 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   if (m == 0 || win == nullptr) return SG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const Win W = to_win(win);
-  // (class, bucket) histogram -> exclusive offsets -> cursors; the small
-  // class comes first in the work array
+  // (class, bucket) histogram -> exclusive offsets -> cursors.  Work array:
+  // [k_bmr small class | k_bmr large class | saved words (k_win)]
+  constexpr int NCLS = 3;
+  const int64_t* bm_off = W.bm_save ? W.bm_off : nullptr;
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(w.bincnt);
-  cudaMemsetAsync(cnt, 0, 2 * NBUCKET * sizeof(unsigned long long), s);
-  k_win_counts<<<grid_for(m, 256), 256, 0, s>>>(m, b_ncols, W.off, W.wins, W.nwin, span_hi, out_off, cnt);
+  cudaMemsetAsync(cnt, 0, NCLS * NBUCKET * sizeof(unsigned long long), s);
+  k_win_counts<<<grid_for(m, 256), 256, 0, s>>>(m, b_ncols, W.off, W.wins, W.nwin, span_hi, out_off, bm_off, cnt);
   if (int rc = check_cuda("k_win_counts")) return rc;
-  unsigned long long h[2 * NBUCKET];
+  unsigned long long h[NCLS * NBUCKET];
   cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric sync", 0);
-  int64_t nwork = 0, nsmall = 0;
-  unsigned long long cur[2 * NBUCKET];
-  for (int c : {1, 0}) {
+  int64_t nwork = 0, nsmall = 0, nrebuild = 0;
+  unsigned long long cur[NCLS * NBUCKET];
+  for (int c : {1, 0, 2}) {
     for (int i = 0; i < NBUCKET; ++i) {
       cur[c * NBUCKET + i] = (unsigned long long)nwork;
       nwork += (int64_t)h[c * NBUCKET + i];
     }
     if (c == 1) nsmall = nwork;
+    if (c == 0) nrebuild = nwork;
   }
   if (nwork == 0) return SG_OK;
   int64_t nnz_a = 0;
@@ -3268,8 +3286,7 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
   }
   cudaMemcpyAsync(cnt, cur, sizeof(cur), cudaMemcpyHostToDevice, s);
   k_win_scatter<<<grid_for(m, 256), 256, 0, s>>>(m, b_ncols, a_ptr, span_lo, span_hi, W.off, W.wins, W.nwin,
-                                                 out_off, W.bm_save ? W.bm_off : nullptr,
-                                                 W.bm_save ? wsc.hcnt : nullptr, cnt, work);
+                                                 out_off, bm_off, W.bm_save ? wsc.hcnt : nullptr, cnt, work);
   if (int rc = check_cuda("k_win_scatter")) return rc;
   if (const char* dump = getenv("SG_DUMP_WINDOWS")) {
     // analysis hook: the window work items as raw 48-byte records
@@ -3282,14 +3299,15 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
     }
   }
   // tickets live after the cursors (the host copy above must finish first)
-  unsigned long long* tickets = cnt + 2 * NBUCKET;
-  cudaMemsetAsync(tickets, 0, 2 * sizeof(unsigned long long), s);
-  ktimer_begin(W.bm_save ? "k_win" : "k_bmr", s);
-  if (W.bm_save) {
-    // saved bitmaps: the warp-specialised window kernel takes every window
-    // (both size classes, in ticket order), heavy entries only
-    int rc = dtype == SG_F64 ? launch_kwin<double>(nwork, work, A, B, bt, W, wsc.hent, out_col, out_val, tickets, s)
-                             : launch_kwin<float>(nwork, work, A, B, bt, W, wsc.hent, out_col, out_val, tickets, s);
+  unsigned long long* tickets = cnt + NCLS * NBUCKET;
+  cudaMemsetAsync(tickets, 0, 3 * sizeof(unsigned long long), s);
+  if (nwork > nrebuild) {
+    // saved words: the warp-specialised window kernel, heavy entries only
+    ktimer_begin("k_win", s);
+    int rc = dtype == SG_F64 ? launch_kwin<double>(nwork - nrebuild, work + nrebuild, A, B, bt, W, wsc.hent, out_col,
+                                                   out_val, tickets, s)
+                             : launch_kwin<float>(nwork - nrebuild, work + nrebuild, A, B, bt, W, wsc.hent, out_col,
+                                                  out_val, tickets, s);
     if (rc) return rc;
     ktimer_end(s);
     // then the light entries add on top of the stored window values
@@ -3298,25 +3316,26 @@ int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_pt
                            : launch_light<float>(m, A, B, W, span_lo, out_off, wsc, out_val, s);
       if (rc) return rc;
     }
-    if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric end", 0);
-    return SG_OK;
   }
-  if (nsmall > 0 && !W.bm_save) {
+  // windows without saved words (no room for them, or thin rows): k_bmr
+  // rebuilds their keys
+  if (nrebuild > 0) ktimer_begin("k_bmr", s);
+  if (nsmall > 0) {
     int rc = dtype == SG_F64
                  ? launch_bmr<double, SMALL_NT, SMALL_WORDS, SMALL_R, 2>(nsmall, work, A, B, bt, W, out_col, out_val,
-                                                                           tickets, s)
+                                                                           tickets + 1, s)
                  : launch_bmr<float, SMALL_NT, SMALL_WORDS, SMALL_R, 2>(nsmall, work, A, B, bt, W, out_col, out_val,
-                                                                          tickets, s);
+                                                                          tickets + 1, s);
     if (rc) return rc;
   }
-  if (nwork > nsmall) {
-    int rc = dtype == SG_F64 ? launch_bmr<double, WIN_NT, WIN_WORDS, WIN_R, 1>(nwork - nsmall, work + nsmall, A, B,
-                                                                                bt, W, out_col, out_val, tickets + 1, s)
-                             : launch_bmr<float, WIN_NT, WIN_WORDS, WIN_R, 1>(nwork - nsmall, work + nsmall, A, B, bt,
-                                                                               W, out_col, out_val, tickets + 1, s);
+  if (nrebuild > nsmall) {
+    int rc = dtype == SG_F64 ? launch_bmr<double, WIN_NT, WIN_WORDS, WIN_R, 1>(nrebuild - nsmall, work + nsmall, A, B,
+                                                                                bt, W, out_col, out_val, tickets + 2, s)
+                             : launch_bmr<float, WIN_NT, WIN_WORDS, WIN_R, 1>(nrebuild - nsmall, work + nsmall, A, B,
+                                                                               bt, W, out_col, out_val, tickets + 2, s);
     if (rc) return rc;
   }
-  ktimer_end(s);
+  if (nrebuild > 0) ktimer_end(s);
   // `cur` (host) is read by the async copy above: keep it alive until done
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_cuda("sg_window_numeric end", 0);
   return SG_OK;
