@@ -166,10 +166,10 @@ int sg_symbolic(int64_t m, int64_t b_ncols, const int64_t* a_ptr, const int32_t*
 /* Long-row numeric pass over the recorded windows, work grouped by column
  * range so concurrent CTAs share B-row slabs in L2; values accumulated in
  * shared memory (fp64) and written sorted at out_off[row] + rank (out_off =
- * row_ptr of C).  With saved bitmaps: the columns are written by a streaming
- * expansion, the values by the warp-specialised window kernel (heavy B rows)
- * and fire-and-forget REDs at the saved ranks (light B rows, < 256 entries);
- * without: one CTA per window rebuilds the window's keys.  work_buf: scratch
+ * row_ptr of C).  Windows of rows with saved words: the warp-specialised
+ * window kernel writes their columns (from the words) and values (optional
+ * SG_LIGHT_LEN: light B rows through REDs at the saved ranks instead); other
+ * windows: one CTA per window rebuilds the window's keys.  work_buf: scratch
  * of work_cap >= sg_window_work_bytes(m, nnz(A), total windows) bytes. */
 int sg_window_numeric(int64_t m, int64_t b_ncols, int dtype, const int64_t* a_ptr,
                       const int32_t* a_col, const void* a_val, const int64_t* b_ptr,
