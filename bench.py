@@ -462,7 +462,10 @@ def main():
                                                  run_shard)
         A0 = to_device(a, dev, dt) if rank == 0 else None
         B0 = (A0 if same else to_device(b, dev, dt)) if rank == 0 else None
-        budget = args.batch_products or (4e9 if a.nnz > 50_000_000 else None)
+        # (only the root holds the inputs: it decides whether rows are batched)
+        big = [a is not None and a.nnz > 50_000_000]
+        dist.broadcast_object_list(big, src=0)
+        budget = args.batch_products or (4e9 if big[0] else None)
         plan = plan_shards(A0, B0, device=dev, products_fn=gpu_products_fn(dev),
                            decide_fn=gpu_decide_fn(cfg, dev), batch_products=budget)
         del A0, B0
