@@ -147,3 +147,25 @@ def test_gpu_sharded_batched_with_global_decision(case):
             if c.stride == 1:
                 np.testing.assert_allclose(vv, cv[cp[lo]:cp[hi]], rtol=1e-12, atol=0)
     assert nb > 2
+
+
+def test_bench_torchrun_two_ranks_one_gpu():
+    """The driver's multi-GPU bench launch (torchrun, rank 0 alone holds the
+    inputs), both arms, with two ranks on cuda:0 over gloo."""
+    import json
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SG_BENCH_SAME_DEVICE="1", SG_BENCH_BACKEND="gloo")
+    for extra in ([], ["--impl", "reference"]):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+               "--config", "rmat12", "--steps", "2", "--warmup", "3", "--no-e2e"] + extra
+        r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+        assert line["n_gpus"] == 2 and line["value"] > 0
+        if not extra:
+            assert line["config"]["nnz_c"] > 0
